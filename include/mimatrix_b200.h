@@ -1,0 +1,108 @@
+/*
+ * mimatrix_b200.h -- C ABI of the B200-native all-pairs binary mutual
+ * information engine (libmimatrix_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA C++ types in the
+ * signatures (`stream` is a cudaStream_t passed as void*, NULL = default).
+ * Every function returns MI_OK (0) or an MI_ERR_* code; the message for the
+ * last failure on the calling thread is available from mi_last_error().
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/mimatrix/):
+ *   mi_all_pairs_host   engine.py:144-168   mi_all_pairs(data, cfg, backend, threads)
+ *                                           (dense path; float64 m x m result)
+ *   mi_gram_ones_host   _kernels.py:48-61   gram_ones_kernel(words, out) / gram.py:56-65
+ *   mi_column_sums_host binmat.py:175-177   column_sums(matrix)
+ *   mi_unpack_colsum    binmat.py:175-177 + the per-column word streams that
+ *                                           _kernels.py:36-45 reads
+ *   mi_gram_mi          _kernels.py:48-61 + gram.py:88-111 + engine.py:93-141
+ *                                           (G11, closed-form counts, MI; fused)
+ *   mi_generate_words   datagen.py:44-73    generate(GenSpec) stream, packed
+ * Error codes mirror the reference's exception classes (errors.py:8-25).
+ */
+#ifndef MIMATRIX_B200_H
+#define MIMATRIX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MI_B200_ABI_VERSION 1
+
+/* return codes (errors.py:8-25) */
+#define MI_OK 0
+#define MI_ERR_DIMENSION 1   /* DimensionError   */
+#define MI_ERR_DOMAIN 2      /* DomainError      */
+#define MI_ERR_CONSISTENCY 3 /* ConsistencyError */
+#define MI_ERR_CUDA 4        /* device / driver failure (MiMatrixError) */
+#define MI_ERR_UNSUPPORTED 5 /* not an sm_100 device, or no device   */
+
+/* engine modes (engine.py:28, EngineConfig.mode) */
+#define MI_MODE_EXACT 0
+#define MI_MODE_EPSILON 1
+
+/* output kinds for mi_gram_mi / mi_all_pairs_host */
+#define MI_OUT_COUNTS 0 /* int32 G11 (debug export, bit-exact parity)  */
+#define MI_OUT_F64 1    /* float64 MI (the reference's MIMatrix.values) */
+#define MI_OUT_F32 2    /* float32 MI (device API, 1e-6 contract)       */
+
+int mi_b200_abi_version(void);
+const char* mi_last_error(void);
+/* number of SMs and compute capability of `device`; MI_ERR_UNSUPPORTED if absent */
+int mi_device_info(int device, int* num_sms, int* cc_major, int* cc_minor);
+
+/* ---- layout helpers (host only, no device needed) ---- */
+/* padded row count N_pad of the K-major operand (bytes per operand row) */
+int64_t mi_kmajor_ld(int64_t n_rows);
+/* padded column count m_pad (operand rows, multiple of the tile size) */
+int64_t mi_kmajor_rows(int64_t n_cols);
+/* output tile edge (256: a 2-SM tcgen05 tile) */
+int mi_tile_size(void);
+/* number of upper-triangle tiles (I <= J) for m columns */
+int64_t mi_num_tiles(int64_t n_cols);
+/* Fill `tiles_out` with the (I, J) pairs (int32 x 2 each) that rank `rank` of
+ * `world` computes, in L2-friendly banded order (`band` tile rows per band,
+ * <= 0 for the default).  Returns the count (or -MI_ERR_* on error); pass
+ * tiles_out = NULL to query the count. */
+int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* tiles_out,
+                     int64_t capacity);
+
+/* ---- device-pointer entry points, enqueued on `stream` ---- */
+/* words (m x nw uint64, nw = ceil(n_rows/64)) -> kmajor (m_pad x ld int8) and
+ * colsum (m_pad int32; padding columns get 0). */
+int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor,
+                     int64_t ld, int32_t* d_colsum, void* stream);
+/* Fused G11 + MI over the listed upper-triangle tiles; writes each tile and
+ * its mirror into d_out (row-major, pitch ld_out elements). */
+int mi_gram_mi(const int8_t* d_kmajor, const int32_t* d_colsum, int64_t n_rows, int64_t n_cols,
+               int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
+               int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
+/* Packed words of a synthetic dataset.  col_kind[c]: 0 Bernoulli(col_threshold[c]),
+ * 1 all zero, 2 all one, 3 col_src[c] XOR Bernoulli(flip_threshold) drawn
+ * with flip_seed.  Thresholds are ceil(p * 2^64) (datagen.py:53-55). */
+int mi_generate_words(uint64_t* d_words, int64_t n_rows, int64_t n_cols, uint64_t seed,
+                      const uint64_t* d_col_threshold, const uint8_t* d_col_kind,
+                      const int32_t* d_col_src, uint64_t flip_threshold, uint64_t flip_seed,
+                      void* stream);
+
+/* ---- host-buffer entry points (H2D, compute, D2H inside; blocking) ---- */
+/* engine.mi_all_pairs(dense): h_out is n_cols x n_cols, float64 (MI_OUT_F64)
+ * or float32 (MI_OUT_F32). */
+int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,
+                      double epsilon, int include_diagonal, int out_kind, void* h_out, int device);
+/* _kernels.gram_ones_kernel(words, out): words is n_cols x n_words; out is
+ * n_cols x n_cols int64 (both triangles, diagonal = column sums). */
+int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, int64_t* h_out,
+                      int device);
+/* binmat.column_sums(matrix) */
+int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, uint64_t* h_out,
+                        int device);
+/* release the cached device workspaces of mi_*_host */
+void mi_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIMATRIX_B200_H */

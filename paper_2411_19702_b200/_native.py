@@ -1,0 +1,125 @@
+"""ctypes binding of libmimatrix_b200.so (C ABI: include/mimatrix_b200.h).
+
+The library is built in-tree (``make -C paper_2411_19702_b200/csrc`` or
+``__graft_entry__.build()``).  There is no fallback: if it is missing or the
+device is not an sm_100 part, every compute call raises NativeError.
+ctypes releases the GIL for the duration of each call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+from .errors import ConsistencyError, DimensionError, DomainError, MiMatrixError, NativeError
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmimatrix_b200.so"
+HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "mimatrix_b200.h"
+
+MI_OK = 0
+MI_ERR_DIMENSION = 1
+MI_ERR_DOMAIN = 2
+MI_ERR_CONSISTENCY = 3
+MI_ERR_CUDA = 4
+MI_ERR_UNSUPPORTED = 5
+
+MI_MODE_EXACT = 0
+MI_MODE_EPSILON = 1
+MI_OUT_COUNTS = 0
+MI_OUT_F64 = 1
+MI_OUT_F32 = 2
+
+_ERRORS = {
+    MI_ERR_DIMENSION: DimensionError,
+    MI_ERR_DOMAIN: DomainError,
+    MI_ERR_CONSISTENCY: ConsistencyError,
+    MI_ERR_CUDA: NativeError,
+    MI_ERR_UNSUPPORTED: NativeError,
+}
+
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_vp = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+_dbl = ctypes.c_double
+
+# name -> (restype, argtypes); must cover every function in include/mimatrix_b200.h
+SIGNATURES = {
+    "mi_b200_abi_version": (_int, []),
+    "mi_last_error": (ctypes.c_char_p, []),
+    "mi_device_info": (_int, [_int, _vp, _vp, _vp]),
+    "mi_kmajor_ld": (_i64, [_i64]),
+    "mi_kmajor_rows": (_i64, [_i64]),
+    "mi_tile_size": (_int, []),
+    "mi_num_tiles": (_i64, [_i64]),
+    "mi_tile_list": (_i64, [_i64, _int, _int, _int, _vp, _i64]),
+    "mi_unpack_colsum": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "mi_gram_mi": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
+    "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
+    "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
+    "mi_gram_ones_host": (_int, [_vp, _i64, _i64, _vp, _int]),
+    "mi_column_sums_host": (_int, [_vp, _i64, _i64, _vp, _int]),
+    "mi_release_workspace": (None, []),
+}
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Function names declared in include/mimatrix_b200.h."""
+    text = HEADER_PATH.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return re.findall(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\*?\s*(mi_[a-z0-9_]+)\s*\(", text, flags=re.M)
+
+
+def lib() -> ctypes.CDLL:
+    """Load the engine library (once).  Raises NativeError when it is absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise NativeError(
+                f"{LIB_PATH} is missing: build it with `make -C paper_2411_19702_b200/csrc` "
+                "(there is no CPU fallback)")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if handle.mi_b200_abi_version() != 1:
+            raise NativeError("libmimatrix_b200.so ABI version mismatch")
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().mi_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != MI_OK:
+        cls = _ERRORS.get(rc, MiMatrixError)
+        raise cls(f"{what}: {last_error()}" if what else last_error())
+
+
+def device_info(device: int) -> tuple[int, int, int]:
+    sms, major, minor = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    check(lib().mi_device_info(device, ctypes.byref(sms), ctypes.byref(major), ctypes.byref(minor)),
+          "mi_device_info")
+    return sms.value, major.value, minor.value
+
+
+def tile_list(n_cols: int, rank: int = 0, world: int = 1, band: int = 0):
+    """(I, J) upper-triangle tiles of `rank` (host-side logic only)."""
+    import numpy as np
+
+    L = lib()
+    count = L.mi_tile_list(n_cols, rank, world, band, None, 0)
+    if count < 0:
+        check(-count, "mi_tile_list")
+    out = np.zeros((max(count, 1), 2), dtype=np.int32)
+    got = L.mi_tile_list(n_cols, rank, world, band, out.ctypes.data, count)
+    if got < 0:
+        check(-got, "mi_tile_list")
+    return out[:got]

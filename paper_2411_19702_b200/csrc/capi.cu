@@ -1,0 +1,427 @@
+// C-ABI layer of libmimatrix_b200.so (declared in include/mimatrix_b200.h).
+// Validation and error codes follow the reference's exception contract
+// (errors.py:8-25, engine.py:36-44,157-158, binmat.py:71-80, gram.py:98-110).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/mimatrix_b200.h"
+#include "mi_kernels.h"
+
+using namespace mib200;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(MI_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define MI_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// Production tile: 256 x 256 on a CTA pair (cta_group::2).  MI_B200_CTA_GROUP=1
+// selects the single-SM 128 x 128 variant (debug / comparison only).
+int cta_group() {
+    static const int cg = [] {
+        const char* e = getenv("MI_B200_CTA_GROUP");
+        return (e && e[0] == '1') ? 1 : 2;
+    }();
+    return cg;
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct DevInfo {
+    int num_sms = 0;
+    int major = 0;
+    int minor = 0;
+};
+
+std::mutex g_info_mu;
+DevInfo g_info[64];
+
+int query_device(int device, DevInfo* out) {
+    if (device < 0 || device >= 64) return fail(MI_ERR_UNSUPPORTED, "bad device ordinal %d", device);
+    std::lock_guard<std::mutex> lk(g_info_mu);
+    DevInfo& d = g_info[device];
+    if (d.num_sms == 0) {
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n <= device)
+            return fail(MI_ERR_UNSUPPORTED, "no CUDA device %d (%s)", device,
+                        e == cudaSuccess ? "not present" : cudaGetErrorString(e));
+        MI_CUDA(cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, device));
+        MI_CUDA(cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, device));
+        MI_CUDA(cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, device));
+    }
+    *out = d;
+    if (d.major != 10 || d.minor != 0)
+        return fail(MI_ERR_UNSUPPORTED, "device %d is sm_%d%d; this engine is built for sm_100a only",
+                    device, d.major, d.minor);
+    return MI_OK;
+}
+
+int current_device_info(DevInfo* out) {
+    int dev = 0;
+    MI_CUDA(cudaGetDevice(&dev));
+    return query_device(dev, out);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int get_encode(PFN_cuTensorMapEncodeTiled_v12000* fn) {
+    std::call_once(g_encode_once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!g_encode) return fail(MI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    *fn = g_encode;
+    return MI_OK;
+}
+
+// K-major int8 operand X (m_pad rows of ld bytes) as a 2-D TMA tensor:
+// 128 x 128-byte boxes, 128B swizzle (matches the UMMA descriptors).
+int make_tmap(CUtensorMap* tm, const int8_t* x, int64_t ld, int64_t m_pad) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc;
+    int rc = get_encode(&enc);
+    if (rc) return rc;
+    cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)m_pad};
+    cuuint64_t gstride[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(x), gdim, gstride, box,
+                     estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MI_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+    return MI_OK;
+}
+
+int check_shape(int64_t n_rows, int64_t n_cols) {
+    if (n_rows < 1 || n_cols < 1)
+        return fail(MI_ERR_DIMENSION, "matrix must have at least one row and one column");
+    if (n_rows > 0x7FFFFFFFLL) return fail(MI_ERR_DIMENSION, "n_rows %lld exceeds 2^31-1", (long long)n_rows);
+    if (n_cols > 0x7FFFFFFFLL) return fail(MI_ERR_DIMENSION, "n_cols %lld exceeds 2^31-1", (long long)n_cols);
+    return MI_OK;
+}
+
+int check_mode(int mode, double eps, int out_kind) {
+    if (mode != MI_MODE_EXACT && mode != MI_MODE_EPSILON)
+        return fail(MI_ERR_DOMAIN, "mode must be exact (0) or epsilon (1), got %d", mode);
+    if (!(eps > 0.0)) return fail(MI_ERR_DOMAIN, "epsilon must be positive, got %g", eps);
+    if (out_kind != MI_OUT_COUNTS && out_kind != MI_OUT_F64 && out_kind != MI_OUT_F32)
+        return fail(MI_ERR_DOMAIN, "unknown output kind %d", out_kind);
+    return MI_OK;
+}
+
+// binmat.py:78-80: padding bits beyond the last row must be zero
+int check_padding(const uint64_t* h_words, int64_t n_rows, int64_t n_cols) {
+    const int64_t nw = (n_rows + 63) / 64;
+    const int rem = (int)(n_rows % 64);
+    if (rem == 0) return MI_OK;
+    const uint64_t pad = ~((1ull << rem) - 1ull);
+    for (int64_t c = 0; c < n_cols; ++c)
+        if (h_words[c * nw + nw - 1] & pad)
+            return fail(MI_ERR_DOMAIN, "padding bits beyond the last row must be zero (column %lld)",
+                        (long long)c);
+    return MI_OK;
+}
+
+// Banded upper-triangle order: within a band of `band` tile rows, sweep J and
+// then the band's rows, so tiles that run concurrently share operand blocks.
+std::vector<int32_t> all_tiles(int64_t T, int band) {
+    std::vector<int32_t> v;
+    v.reserve((size_t)(T * (T + 1)));
+    for (int64_t I0 = 0; I0 < T; I0 += band)
+        for (int64_t J = I0; J < T; ++J)
+            for (int64_t I = I0; I < I0 + band && I <= J; ++I) {
+                v.push_back((int32_t)I);
+                v.push_back((int32_t)J);
+            }
+    return v;
+}
+
+// Grow-only device workspace for the host-buffer entry points.
+struct Workspace {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    void* words = nullptr; size_t words_cap = 0;
+    void* x = nullptr; size_t x_cap = 0;
+    void* colsum = nullptr; size_t colsum_cap = 0;
+    void* tiles = nullptr; size_t tiles_cap = 0;
+    void* out = nullptr; size_t out_cap = 0;
+};
+std::mutex g_ws_mu;
+Workspace g_ws[64];
+
+int ensure(void** p, size_t* cap, size_t need) {
+    if (*cap >= need && *p) return MI_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    MI_CUDA(cudaMalloc(p, need ? need : 16));
+    *cap = need;
+    return MI_OK;
+}
+
+void release(Workspace& w) {
+    if (w.device < 0) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(w.device);
+    void** ps[] = {&w.words, &w.x, &w.colsum, &w.tiles, &w.out};
+    for (void** p : ps)
+        if (*p) cudaFree(*p), *p = nullptr;
+    w.words_cap = w.x_cap = w.colsum_cap = w.tiles_cap = w.out_cap = 0;
+    if (w.stream) cudaStreamDestroy(w.stream), w.stream = nullptr;
+    w.device = -1;
+    cudaSetDevice(prev);
+}
+
+// words (host) -> X, colsum on the device; shared by the host entry points.
+int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int64_t* ld_out,
+                 int64_t* m_pad_out, const DevInfo& info) {
+    const int64_t nw = (n_rows + 63) / 64;
+    const int64_t ld = mi_kmajor_ld(n_rows);
+    const int64_t m_pad = mi_kmajor_rows(n_cols);
+    int rc;
+    if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
+    if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
+    MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
+    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
+                                 (int32_t*)ws.colsum, info.num_sms, ws.stream));
+    *ld_out = ld;
+    *m_pad_out = m_pad;
+    return MI_OK;
+}
+
+int workspace_for(int device, Workspace** out, DevInfo* info) {
+    int rc = query_device(device, info);
+    if (rc) return rc;
+    MI_CUDA(cudaSetDevice(device));
+    Workspace& ws = g_ws[device];
+    if (ws.device < 0) {
+        ws.device = device;
+        MI_CUDA(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+    }
+    *out = &ws;
+    return MI_OK;
+}
+
+int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t m_pad, int mode, double eps,
+              int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const DevInfo& info) {
+    (void)m_pad;
+    const int64_t n_tiles = mi_num_tiles(n_cols);
+    std::vector<int32_t> tiles = all_tiles(mi_kmajor_rows(n_cols) / mi_tile_size(), 8);
+    int rc;
+    if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
+    MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
+    (void)info;
+    return mi_gram_mi((const int8_t*)ws.x, (const int32_t*)ws.colsum, n_rows, n_cols, ld, mode, eps,
+                      include_diagonal, out_kind, d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, ws.stream);
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+extern "C" {
+
+int mi_b200_abi_version(void) { return MI_B200_ABI_VERSION; }
+
+const char* mi_last_error(void) { return g_err; }
+
+int mi_device_info(int device, int* num_sms, int* cc_major, int* cc_minor) {
+    DevInfo d;
+    int rc = query_device(device, &d);
+    if (num_sms) *num_sms = d.num_sms;
+    if (cc_major) *cc_major = d.major;
+    if (cc_minor) *cc_minor = d.minor;
+    return rc;
+}
+
+int64_t mi_kmajor_ld(int64_t n_rows) { return round_up(n_rows < 1 ? 1 : n_rows, 128); }
+
+int64_t mi_kmajor_rows(int64_t n_cols) { return round_up(n_cols < 1 ? 1 : n_cols, 256); }
+
+int mi_tile_size(void) { return gram_mi_tile_size(cta_group()); }
+
+int64_t mi_num_tiles(int64_t n_cols) {
+    const int64_t T = mi_kmajor_rows(n_cols) / mi_tile_size();
+    return T * (T + 1) / 2;
+}
+
+int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* tiles_out, int64_t capacity) {
+    if (n_cols < 1) return -fail(MI_ERR_DIMENSION, "n_cols must be >= 1");
+    if (world < 1 || rank < 0 || rank >= world)
+        return -fail(MI_ERR_DOMAIN, "bad rank %d of world %d", rank, world);
+    if (band <= 0) band = 8;
+    const int64_t T = mi_kmajor_rows(n_cols) / mi_tile_size();
+    std::vector<int32_t> all = all_tiles(T, band);
+    const int64_t total = (int64_t)all.size() / 2;
+    int64_t count = 0;
+    for (int64_t g = rank; g < total; g += world) {
+        if (tiles_out) {
+            if (count >= capacity) return -fail(MI_ERR_DIMENSION, "tile buffer too small");
+            tiles_out[2 * count] = all[2 * g];
+            tiles_out[2 * count + 1] = all[2 * g + 1];
+        }
+        ++count;
+    }
+    return count;
+}
+
+int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor, int64_t ld,
+                     int32_t* d_colsum, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (ld < mi_kmajor_ld(n_rows) || ld % 128)
+        return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
+                    (long long)mi_kmajor_ld(n_rows));
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    const int64_t nw = (n_rows + 63) / 64;
+    MI_CUDA(launch_unpack_colsum(d_words, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
+                                 info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
+}
+
+int mi_gram_mi(const int8_t* d_kmajor, const int32_t* d_colsum, int64_t n_rows, int64_t n_cols, int64_t ld,
+               int mode, double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
+               const int32_t* d_tiles, int64_t n_tiles, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
+    if (ld < mi_kmajor_ld(n_rows) || ld % 128)
+        return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
+                    (long long)mi_kmajor_ld(n_rows));
+    if (ld_out < n_cols) return fail(MI_ERR_DIMENSION, "ld_out %lld < n_cols", (long long)ld_out);
+    if (n_tiles < 0 || n_tiles > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "bad n_tiles");
+    if (n_tiles == 0) return MI_OK;
+    if (out_kind == MI_OUT_COUNTS && mode != MI_MODE_EXACT)
+        return fail(MI_ERR_DOMAIN, "counts export ignores the mode; pass MI_MODE_EXACT");
+    if ((reinterpret_cast<uintptr_t>(d_kmajor) & 15) != 0)
+        return fail(MI_ERR_DOMAIN, "kmajor operand must be 16-byte aligned");
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    CUtensorMap tm;
+    if ((rc = make_tmap(&tm, d_kmajor, ld, mi_kmajor_rows(n_cols)))) return rc;
+    GramMiParams p;
+    p.colsum = d_colsum;
+    p.tiles = reinterpret_cast<const int2*>(d_tiles);
+    p.n_tiles = (int)n_tiles;
+    p.num_k_blocks = (int)(mi_kmajor_ld(n_rows) / 128);
+    p.n_rows = (int)n_rows;
+    p.m = (int)n_cols;
+    p.ld_out = ld_out;
+    p.out = d_out;
+    p.eps = epsilon;
+    p.include_diagonal = include_diagonal ? 1 : 0;
+    const int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
+    MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tm, p, info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
+}
+
+int mi_generate_words(uint64_t* d_words, int64_t n_rows, int64_t n_cols, uint64_t seed,
+                      const uint64_t* d_col_threshold, const uint8_t* d_col_kind, const int32_t* d_col_src,
+                      uint64_t flip_threshold, uint64_t flip_seed, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    MI_CUDA(launch_generate_words(d_words, n_rows, n_cols, seed, d_col_threshold, d_col_kind, d_col_src,
+                                  flip_threshold, flip_seed, (cudaStream_t)stream));
+    return MI_OK;
+}
+
+int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                      int include_diagonal, int out_kind, void* h_out, int device) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
+    if (out_kind == MI_OUT_COUNTS) return fail(MI_ERR_DOMAIN, "use mi_gram_ones_host for counts");
+    if ((rc = check_padding(h_words, n_rows, n_cols))) return rc;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    DevInfo info;
+    if ((rc = workspace_for(device, &ws, &info))) return rc;
+    int64_t ld, m_pad;
+    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
+    const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * esz;
+    if ((rc = ensure(&ws->out, &ws->out_cap, out_bytes))) return rc;
+    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out,
+                        n_cols, info)))
+        return rc;
+    MI_CUDA(cudaMemcpyAsync(h_out, ws->out, out_bytes, cudaMemcpyDeviceToHost, ws->stream));
+    MI_CUDA(cudaStreamSynchronize(ws->stream));
+    return MI_OK;
+}
+
+int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, int64_t* h_out, int device) {
+    if (n_cols < 1 || n_words < 1) return fail(MI_ERR_DIMENSION, "words must be a non-empty (m, nw) array");
+    const int64_t n_rows = n_words * 64;  // padding bits are zero, so they add nothing
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    DevInfo info;
+    int rc;
+    if ((rc = workspace_for(device, &ws, &info))) return rc;
+    int64_t ld, m_pad;
+    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * 4;
+    if ((rc = ensure(&ws->out, &ws->out_cap, out_bytes))) return rc;
+    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, MI_MODE_EXACT, 1e-12, 1, MI_OUT_COUNTS, ws->out, n_cols,
+                        info)))
+        return rc;
+    std::vector<int32_t> tmp((size_t)n_cols * (size_t)n_cols);
+    MI_CUDA(cudaMemcpyAsync(tmp.data(), ws->out, out_bytes, cudaMemcpyDeviceToHost, ws->stream));
+    MI_CUDA(cudaStreamSynchronize(ws->stream));
+    for (size_t k = 0; k < tmp.size(); ++k) h_out[k] = tmp[k];
+    return MI_OK;
+}
+
+int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, uint64_t* h_out, int device) {
+    if (n_cols < 1 || n_words < 1) return fail(MI_ERR_DIMENSION, "words must be a non-empty (m, nw) array");
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    DevInfo info;
+    int rc;
+    if ((rc = workspace_for(device, &ws, &info))) return rc;
+    int64_t ld, m_pad;
+    if ((rc = stage_inputs(*ws, h_words, n_words * 64, n_cols, &ld, &m_pad, info))) return rc;
+    std::vector<int32_t> tmp((size_t)n_cols);
+    MI_CUDA(cudaMemcpyAsync(tmp.data(), ws->colsum, (size_t)n_cols * 4, cudaMemcpyDeviceToHost, ws->stream));
+    MI_CUDA(cudaStreamSynchronize(ws->stream));
+    for (int64_t k = 0; k < n_cols; ++k) h_out[k] = (uint64_t)tmp[k];
+    return MI_OK;
+}
+
+void mi_release_workspace(void) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& w : g_ws) release(w);
+}
+
+}  // extern "C"

@@ -1,0 +1,42 @@
+// Internal (C++) interface between the C-ABI layer (capi.cu) and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#define MI_OUT_COUNTS 0
+#define MI_OUT_F64 1
+#define MI_OUT_F32 2
+#define MI_MODE_EXACT 0
+#define MI_MODE_EPSILON 1
+
+namespace mib200 {
+
+struct GramMiParams {
+    const int32_t* colsum;  // [m_pad] ones per column (0 for padding columns)
+    const int2* tiles;      // [n_tiles] (I, J) tile coordinates, I <= J
+    int n_tiles;
+    int num_k_blocks;       // N_pad / 128
+    int n_rows;             // N
+    int m;                  // real columns (outputs beyond m are not written)
+    int64_t ld_out;         // output row pitch in elements
+    void* out;              // int32 / double / float, row-major m x ld_out
+    double eps;
+    int include_diagonal;
+};
+
+cudaError_t launch_gram_mi(int cg, int out_kind, int mode, const CUtensorMap& tmap,
+                           const GramMiParams& p, int num_sms, cudaStream_t stream);
+int gram_mi_tile_size(int cg);
+uint32_t gram_mi_smem_bytes();
+
+cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t m, int64_t nw, int8_t* x,
+                                 int64_t ld, int64_t m_pad, int32_t* colsum, int num_sms,
+                                 cudaStream_t stream);
+
+cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,
+                                  const uint64_t* col_threshold, const uint8_t* col_kind,
+                                  const int32_t* col_src, uint64_t flip_threshold,
+                                  uint64_t flip_seed, cudaStream_t stream);
+
+}  // namespace mib200

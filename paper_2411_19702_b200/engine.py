@@ -1,0 +1,260 @@
+"""All-pairs binary mutual information on B200 -- the drop-in entry point.
+
+``mi_all_pairs(data, cfg=None, backend="dense", threads=0) -> MIMatrix`` keeps
+the reference's signature, defaults, output layout (fresh C-contiguous m x m
+float64, bit-identical symmetric, diagonal = column entropy) and error
+behaviour (engine.py:144-168 of /root/reference/pkg/src/mimatrix).  Its body
+is: H2D of the packed words -> kernel 1 (unpack + column sums) -> kernel 2+3
+(tcgen05 int8 Gram over upper-triangle tiles with the MI epilogue fused on the
+TMEM accumulators) -> D2H.  All three backends of the reference run this one
+GPU path (there is no CPU fallback and no multi-backend dispatch); the
+backend name is still validated exactly like the reference does.
+
+``MIEngine`` is the device API: device-resident inputs and outputs (torch
+tensors, used only as device memory and streams), float32 or float64 output,
+tile subsets for the multi-GPU dispatcher, and the int32 count export used for
+bit-exact parity.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .binmat import as_dense_words, n_words
+from .errors import DimensionError, DomainError, NativeError
+
+MODES = ("exact", "epsilon")
+BACKENDS = ("dense", "sparse", "direct")
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """Evaluation options for MI assembly (engine.py:32-44)."""
+
+    mode: str = "exact"
+    epsilon: float = 1e-12
+    include_diagonal: bool = True
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise DomainError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if not self.epsilon > 0:
+            raise DomainError(f"epsilon must be positive, got {self.epsilon}")
+
+
+@dataclass(frozen=True, eq=False)
+class MIMatrix:
+    """Symmetric m x m matrix of pairwise mutual information, in bits (engine.py:66-78)."""
+
+    values: np.ndarray
+
+    @property
+    def n_cols(self) -> int:
+        return self.values.shape[0]
+
+    def checksum(self) -> float:
+        return float(self.values.sum())
+
+
+def _config_fields(cfg) -> tuple[int, float, int]:
+    """Accept our EngineConfig or the reference's (same fields)."""
+    if cfg is None:
+        cfg = EngineConfig()
+    mode = getattr(cfg, "mode", None)
+    eps = getattr(cfg, "epsilon", None)
+    if mode not in MODES:
+        raise DomainError(f"mode must be one of {MODES}, got {mode!r}")
+    if eps is None or not eps > 0:
+        raise DomainError(f"epsilon must be positive, got {eps}")
+    return MODES.index(mode), float(eps), int(bool(getattr(cfg, "include_diagonal", True)))
+
+
+_OUT_KIND = {torch.float64: nat.MI_OUT_F64, torch.float32: nat.MI_OUT_F32, torch.int32: nat.MI_OUT_COUNTS}
+
+
+@dataclass
+class Prepared:
+    """Device-resident operand of one dataset: K-major int8 X and column sums."""
+
+    n_rows: int
+    n_cols: int
+    ld: int          # bytes per X row (N_pad)
+    m_pad: int       # X rows
+    x: torch.Tensor  # int8 (m_pad, ld)
+    colsum: torch.Tensor  # int32 (m_pad,)
+
+
+def _stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class MIEngine:
+    """Per-device engine.  Allocation goes through torch's caching allocator;
+    kernels are enqueued on torch's current stream of that device."""
+
+    _instances: dict[int, "MIEngine"] = {}
+    _lock = threading.Lock()
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise NativeError("no CUDA device visible: the MI engine runs only on B200 (sm_100a)")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device if isinstance(device, int) else device.index or 0)
+        self.num_sms, major, minor = nat.device_info(self.device.index)
+        self._tiles: dict[tuple, torch.Tensor] = {}
+
+    @classmethod
+    def get(cls, device: int | torch.device | None = None) -> "MIEngine":
+        if device is None:
+            if not torch.cuda.is_available():
+                raise NativeError("no CUDA device visible: the MI engine runs only on B200 (sm_100a)")
+            device = torch.cuda.current_device()
+        idx = device if isinstance(device, int) else (device.index or 0)
+        with cls._lock:
+            if idx not in cls._instances:
+                cls._instances[idx] = cls(idx)
+            return cls._instances[idx]
+
+    # ------------------------------------------------------------------ layout
+    @staticmethod
+    def layout(n_rows: int, n_cols: int) -> tuple[int, int]:
+        L = nat.lib()
+        return int(L.mi_kmajor_ld(n_rows)), int(L.mi_kmajor_rows(n_cols))
+
+    def tiles(self, n_cols: int, rank: int = 0, world: int = 1) -> torch.Tensor:
+        key = (n_cols, rank, world)
+        t = self._tiles.get(key)
+        if t is None:
+            host = nat.tile_list(n_cols, rank, world)
+            t = torch.from_numpy(np.ascontiguousarray(host)).to(self.device)
+            self._tiles[key] = t
+        return t
+
+    # ------------------------------------------------------------------ stages
+    def upload(self, words: np.ndarray) -> torch.Tensor:
+        """Host words (m, nw) uint64 -> device tensor (int64 storage, same bits)."""
+        host = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))
+        return host.to(self.device, non_blocking=False)
+
+    def prepare(self, words_dev: torch.Tensor, n_rows: int, n_cols: int) -> Prepared:
+        """Kernel 1: unpack the packed columns to the K-major int8 operand and
+        count ones per column (binmat.column_sums)."""
+        nw = n_words(n_rows)
+        if words_dev.device != self.device or words_dev.dtype not in (torch.int64, torch.uint64):
+            raise DimensionError("words must be a 64-bit tensor on the engine's device")
+        if tuple(words_dev.shape) != (n_cols, nw) or not words_dev.is_contiguous():
+            raise DimensionError(f"words must be contiguous with shape {(n_cols, nw)}")
+        ld, m_pad = self.layout(n_rows, n_cols)
+        x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
+        colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
+        nat.check(nat.lib().mi_unpack_colsum(words_dev.data_ptr(), n_rows, n_cols, x.data_ptr(), ld,
+                                             colsum.data_ptr(), _stream_ptr(self.device)),
+                  "mi_unpack_colsum")
+        return Prepared(n_rows, n_cols, ld, m_pad, x, colsum)
+
+    def compute(self, prep: Prepared, cfg=None, out_dtype: torch.dtype = torch.float64,
+                tiles: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Kernels 2+3: fused Gram + MI over `tiles` (all upper-triangle tiles by
+        default), each written with its mirror into `out` (m x m)."""
+        if out_dtype not in _OUT_KIND:
+            raise DomainError(f"out_dtype must be float64, float32 or int32, got {out_dtype}")
+        mode, eps, diag = _config_fields(cfg)
+        kind = _OUT_KIND[out_dtype]
+        if kind == nat.MI_OUT_COUNTS:
+            mode = nat.MI_MODE_EXACT
+        m = prep.n_cols
+        if out is None:
+            out = torch.empty((m, m), dtype=out_dtype, device=self.device)
+        if out.dtype != out_dtype or out.dim() != 2 or out.shape[0] < m or out.shape[1] < m \
+                or out.stride(1) != 1 or out.device != self.device:
+            raise DimensionError("out must be a row-major (>= m, >= m) tensor of out_dtype on the device")
+        if tiles is None:
+            tiles = self.tiles(m)
+        nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colsum.data_ptr(), prep.n_rows, m, prep.ld,
+                                       mode, eps, diag, kind, out.data_ptr(), out.stride(0),
+                                       tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),
+                  "mi_gram_mi")
+        return out
+
+    # ------------------------------------------------------------------ composites
+    def all_pairs_device(self, words_dev: torch.Tensor, n_rows: int, n_cols: int, cfg=None,
+                         out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None) -> torch.Tensor:
+        return self.compute(self.prepare(words_dev, n_rows, n_cols), cfg, out_dtype, out=out)
+
+    def gram_counts(self, words_dev: torch.Tensor, n_rows: int, n_cols: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """Debug export for parity: (G11 int32 m x m, column sums int32 m)."""
+        prep = self.prepare(words_dev, n_rows, n_cols)
+        g = self.compute(prep, None, torch.int32)
+        return g, prep.colsum[:n_cols]
+
+    def all_pairs_host(self, words: np.ndarray | torch.Tensor, n_rows: int, n_cols: int, cfg=None,
+                       out_dtype: torch.dtype = torch.float64, host_out: torch.Tensor | None = None) -> torch.Tensor:
+        """Host words in, host MI out (pinned tensor); H2D and D2H included."""
+        if isinstance(words, np.ndarray):
+            words = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))
+        words_dev = words.to(self.device, non_blocking=words.is_pinned())
+        dev_out = self.all_pairs_device(words_dev, n_rows, n_cols, cfg, out_dtype)
+        if host_out is None:
+            host_out = torch.empty((n_cols, n_cols), dtype=out_dtype, pin_memory=True)
+        host_out.copy_(dev_out, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return host_out
+
+
+def mi_all_pairs(data, cfg: EngineConfig | None = None, backend: str = "dense", threads: int = 0,
+                 device: int | None = None) -> MIMatrix:
+    """Full pairwise MI matrix (drop-in for engine.mi_all_pairs, engine.py:144-168).
+
+    ``backend`` must be one of the reference's names ("dense", "sparse",
+    "direct"); all run the same GPU path.  ``threads`` is accepted and ignored:
+    results are bit-identical regardless of parallelism.
+    """
+    if backend not in BACKENDS:
+        raise DomainError(f"backend must be one of {BACKENDS}, got {backend!r}")
+    _config_fields(cfg)
+    n, m, words = as_dense_words(data)
+    eng = MIEngine.get(device)
+    host = eng.all_pairs_host(words, n, m, cfg, torch.float64)
+    return MIMatrix(values=host.numpy())
+
+
+def gram_ones(data, device: int | None = None) -> np.ndarray:
+    """Drop-in for gram.gram_ones (gram.py:56-65): int64 m x m co-occurring ones."""
+    n, m, words = as_dense_words(data)
+    out = np.empty((m, m), dtype=np.int64)
+    w = np.ascontiguousarray(words)
+    dev = MIEngine.get(device).device.index
+    nat.check(nat.lib().mi_gram_ones_host(w.ctypes.data, m, w.shape[1], out.ctypes.data, dev), "mi_gram_ones_host")
+    return out
+
+
+def column_sums(data, device: int | None = None) -> np.ndarray:
+    """Drop-in for binmat.column_sums (binmat.py:175-177), computed by kernel 1."""
+    n, m, words = as_dense_words(data)
+    out = np.empty((m,), dtype=np.uint64)
+    w = np.ascontiguousarray(words)
+    dev = MIEngine.get(device).device.index
+    nat.check(nat.lib().mi_column_sums_host(w.ctypes.data, m, w.shape[1], out.ctypes.data, dev),
+              "mi_column_sums_host")
+    return out
+
+
+def mi_all_pairs_c_abi(data, cfg: EngineConfig | None = None, device: int = 0,
+                       out_dtype=np.float64) -> np.ndarray:
+    """Same computation through the pure C entry point mi_all_pairs_host (what a
+    non-Python binding would call); used by tests and the e2e cross-check."""
+    mode, eps, diag = _config_fields(cfg)
+    n, m, words = as_dense_words(data)
+    out = np.empty((m, m), dtype=out_dtype)
+    kind = nat.MI_OUT_F64 if out_dtype == np.float64 else nat.MI_OUT_F32
+    w = np.ascontiguousarray(words)
+    nat.check(nat.lib().mi_all_pairs_host(w.ctypes.data, n, m, mode, eps, diag, kind, out.ctypes.data, device),
+              "mi_all_pairs_host")
+    return out
+

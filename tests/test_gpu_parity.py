@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden outputs.
+
+Bar (BASELINE.json / SURVEY 8(c)): co-occurrence counts bit-exact; MI within
+1e-6 absolute of the reference's float64 result (the float64 path is held to
+1e-12 here, the same tolerance the reference's own tests use); exact 1.0 /
+0.0 golden values reproduced exactly; output bit-identically symmetric.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import rand_bits
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+TOL_F64 = 1e-12   # reference's own tolerance for bulk-vs-oracle (test_engine.py:121-140)
+TOL_F32 = 1e-6    # BASELINE contract for the float32 device output
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gpu_counts(engine, words, n):
+    m = words.shape[0]
+    g, v = engine.gram_counts(engine.upload(words), n, m)
+    return g.cpu().numpy().astype(np.int64), v.cpu().numpy().astype(np.uint64)
+
+
+def gpu_mi(engine, words, n, cfg=None, dtype=None):
+    dtype = dtype or torch.float64
+    m = words.shape[0]
+    out = engine.all_pairs_device(engine.upload(words), n, m, cfg, dtype)
+    return out.cpu().numpy()
+
+
+def cfg_of(mode="exact", eps=1e-12, diag=True):
+    from paper_2411_19702_b200 import EngineConfig
+
+    return EngineConfig(mode=mode, epsilon=eps, include_diagonal=diag)
+
+
+# --------------------------------------------------------------- golden cases
+
+def test_counts_bit_exact_on_golden(engine, golden):
+    arrays, meta = golden
+    for name, case in meta["cases"].items():
+        words = arrays[f"{name}/words"]
+        g, v = gpu_counts(engine, words, case["n_rows"])
+        assert np.array_equal(v, arrays[f"{name}/v"]), f"{name}: column sums"
+        assert sha(g) == case["g11_sha256"], f"{name}: G11 differs from reference gram_ones"
+
+
+def test_mi_f64_matches_reference_on_golden(engine, golden):
+    arrays, meta = golden
+    worst = 0.0
+    for name, case in meta["cases"].items():
+        words = arrays[f"{name}/words"]
+        mi = gpu_mi(engine, words, case["n_rows"])
+        assert mi.dtype == np.float64 and mi.shape == (case["n_cols"],) * 2
+        assert np.array_equal(mi, mi.T), f"{name}: not bit-identically symmetric"
+        if case["full"]:
+            ref = arrays[f"{name}/mi"]
+            got = mi
+        else:
+            ii, jj = arrays[f"{name}/sample_i"], arrays[f"{name}/sample_j"]
+            ref, got = arrays[f"{name}/sample_mi"], mi[ii, jj]
+        err = float(np.max(np.abs(got - ref)))
+        worst = max(worst, err)
+        assert err < TOL_F64, f"{name}: max |gpu - ref| = {err}"
+        assert abs(mi.sum() - case["mi_checksum"]) < 1e-9 * max(1.0, case["n_cols"] ** 2)
+    print(f"worst |gpu - reference| over golden cases: {worst:.3e}")
+
+
+def test_mi_variants_on_golden(engine, golden):
+    arrays, meta = golden
+    for name, case in meta["cases"].items():
+        for var in case["variants"]:
+            cfg = cfg_of(var["mode"], var["epsilon"], var["include_diagonal"])
+            mi = gpu_mi(engine, arrays[f"{name}/words"], case["n_rows"], cfg)
+            ref = arrays[f"{name}/mi_{var['name']}"]
+            got = mi if case["full"] else mi[arrays[f"{name}/sample_i"], arrays[f"{name}/sample_j"]]
+            err = float(np.max(np.abs(got - ref)))
+            assert err < TOL_F64, f"{name}/{var['name']}: {err}"
+            if not var["include_diagonal"]:
+                assert np.all(np.diagonal(mi) == 0.0)
+
+
+def test_golden_values_exact(engine, golden):
+    """test_acceptance.py:112-125 / test_engine.py:25,74-93 through the GPU path."""
+    arrays, _ = golden
+    bal = gpu_mi(engine, arrays["balanced_identical/words"], 4)
+    assert bal[0, 1] == 1.0 and bal[1, 0] == 1.0
+    ind = gpu_mi(engine, arrays["independent/words"], 4)
+    assert ind[0, 1] == 0.0
+    gold = gpu_mi(engine, arrays["golden_0011_0111/words"], 4)
+    assert abs(gold[0, 1] - 0.311278124459133) < 1e-12
+    h = gpu_mi(engine, arrays["h075/words"], 4)
+    assert abs(h[0, 0] - 0.811278124459133) < 1e-12
+    one_row = gpu_mi(engine, arrays["single_row/words"], 1)
+    assert np.all(one_row == 0.0)
+
+
+def test_f32_output_within_contract(engine, golden):
+    arrays, meta = golden
+    for name, case in meta["cases"].items():
+        mi = gpu_mi(engine, arrays[f"{name}/words"], case["n_rows"], None, torch.float32)
+        assert mi.dtype == np.float32
+        ref = arrays[f"{name}/mi"] if case["full"] else arrays[f"{name}/sample_mi"]
+        got = mi if case["full"] else mi[arrays[f"{name}/sample_i"], arrays[f"{name}/sample_j"]]
+        assert float(np.max(np.abs(got.astype(np.float64) - ref))) < TOL_F32, name
+
+
+# --------------------------------------------------------------- edge shapes
+
+EDGE_SHAPES = [
+    (1, 1), (1, 300), (2, 257), (63, 255), (64, 256), (65, 257), (127, 511), (128, 512),
+    (129, 513), (255, 300), (256, 129), (1000, 700), (3000, 1025),
+]
+
+
+@pytest.mark.parametrize("n,m", EDGE_SHAPES)
+@pytest.mark.parametrize("density", [0.0, 0.3, 1.0])
+def test_edge_shapes_counts_and_mi(engine, n, m, density):
+    rng = np.random.default_rng(n * 7919 + m + int(density * 10))
+    bits = rand_bits(rng, n, m, density)
+    words = O.pack_bits(bits)
+    g, v = gpu_counts(engine, words, n)
+    assert np.array_equal(v, O.column_sums(words))
+    assert np.array_equal(g, O.c_gram_ones(words))
+    mi = gpu_mi(engine, words, n)
+    ref = O.c_mi_all_pairs(words, n)
+    assert np.array_equal(mi, mi.T)
+    assert float(np.max(np.abs(mi - ref))) < TOL_F64
+
+
+def test_determinism_and_c_abi_host_path(engine):
+    from paper_2411_19702_b200 import BinaryMatrix, mi_all_pairs, mi_all_pairs_c_abi
+
+    rng = np.random.default_rng(99)
+    bits = rand_bits(rng, 2000, 600, 0.4)
+    mat = BinaryMatrix(2000, 600, O.pack_bits(bits))
+    a = mi_all_pairs(mat).values
+    b = mi_all_pairs(mat, threads=1).values
+    c = mi_all_pairs_c_abi(mat)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert a.flags["C_CONTIGUOUS"] and a.dtype == np.float64
+
+
+def test_backends_and_errors(engine):
+    from paper_2411_19702_b200 import BinaryMatrix, DomainError, EngineConfig, mi_all_pairs
+
+    rng = np.random.default_rng(5)
+    mat = BinaryMatrix(100, 9, O.pack_bits(rand_bits(rng, 100, 9, 0.5)))
+    dense = mi_all_pairs(mat, backend="dense").values
+    for b in ("sparse", "direct"):
+        assert np.array_equal(mi_all_pairs(mat, backend=b).values, dense)
+    with pytest.raises(DomainError):
+        mi_all_pairs(mat, backend="gpu")
+    with pytest.raises(DomainError):
+        EngineConfig(mode="fuzzy")
+
+
+# --------------------------------------------------------------- generator
+
+def test_generator_bit_exact(engine, golden):
+    from paper_2411_19702_b200 import datagen
+
+    arrays, meta = golden
+    for key in arrays.files:
+        if not key.startswith("datagen/gen_"):
+            continue
+        parts = key.split("_")
+        n, m = map(int, parts[1].split("x"))
+        seed, dens = int(parts[2][1:]), float(parts[3][1:])
+        w = datagen.generate(n, m, dens, seed, engine.device).cpu().numpy().view(np.uint64)
+        assert np.array_equal(w, arrays[key]), key
+    w1 = datagen.generate(1000, 500, 0.5, 0, engine.device).cpu().numpy().view(np.uint64)
+    assert sha(w1) == meta["datagen"]["cfg1"]["words_sha256"]
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_config_recipes_bit_exact(engine, cfg):
+    from paper_2411_19702_b200 import datagen
+
+    n, m = {1: (1000, 500), 2: (3000, 600), 3: (700, 300), 4: (2000, 1000), 5: (4000, 300)}[cfg]
+    rec = datagen.config_recipe(cfg, n, m)
+    w = datagen.generate_words_device(rec, engine.device).cpu().numpy().view(np.uint64)
+    ref = O.pack_bits(O.generate_config_bits(O.config_recipe(cfg, n, m)))
+    assert np.array_equal(w, ref)
