@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark: all-pairs binary MI throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+A step is one pass of the hot path over one synthetic dataset of the chosen
+BASELINE config (default config 3, N=100,000 x m=10,000, f64 MI): kernel 1
+(unpack + column sums) and kernel 2+3 (tcgen05 int8 Gram with the fused MI
+epilogue) on device-resident packed words, output left on the device
+(sharded across ranks when N>1; the only collective is the broadcast of the
+packed words).  Rank 0 prints one JSON line.  `value` is pair-samples/s
+(N*m(m+1)/2 per step) over the whole job, timed with CUDA events, L2 flushed
+between steps, max over ranks.  `e2e` is the same metric through the public
+API with host (pinned) words in and the host MI matrix out.
+
+`--impl reference` times the reference algorithm on the host CPU cores (the
+C restatement in oracle/, OpenMP, all threads) on a bounded column sample of
+the same workload; it is the driver's reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "all-pairs binary MI: N·m(m+1)/2 pair-samples/s, % int8 tensor roofline, 1–8 GPU"
+UNIT = "pair-samples/s"
+INT8_NOMINAL_TOPS = 4500.0  # B200 dense int8, datasheet
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0, help="target length of the CPU sample")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def pair_samples(n: int, m: int) -> float:
+    return float(n) * m * (m + 1) / 2.0
+
+
+def workload_name(cfg: int, n: int, m: int, out: str) -> str:
+    desc = {1: "Bernoulli(0.5) + 2 all-zero + 2 all-one columns, seed 0",
+            2: "p_c~U(0.05,0.95), 200 planted noisy copies (flip 0.1), seed 1",
+            3: "Bernoulli(0.5), seed 2",
+            4: "p_c~Beta(0.5,20), 1% noisy copies (flip 0.05), seed 3",
+            5: "p_c~U(0.01,0.99), seed 4"}[cfg]
+    return f"config {cfg}: N={n:,} x m={m:,} {desc}; {out} MI"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in Path(self.path).read_text().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    smax.append(float(f[2]))
+                    power.append(float(f[3]))
+                except ValueError:
+                    continue
+                for name, val in zip(names, f[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        finally:
+            os.unlink(self.path)
+        loaded = [s for s, p in zip(sm, power) if p > 250.0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(loaded),
+                "power_w_max": max(power) if power else None}
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_sample(cfg: int, target_s: float, max_cols: int | None = None):
+    """Time the C restatement of the reference on a column sample of the
+    config, sized to ~target_s seconds.  Returns (value pair-samples/s, info)."""
+    from oracle import oracle as O
+
+    rec = O.config_recipe(cfg)
+    n, m = rec["n"], rec["m"]
+    threads = O.c_num_threads()
+    rng = __import__("numpy").random.default_rng(1234)
+
+    def run(ms):
+        cols = sorted(rng.choice(m, ms, replace=False).tolist()) if ms < m else None
+        words = O.c_generate_config_words(rec, cols)
+        t0 = time.perf_counter()
+        O.c_mi_all_pairs(words, n)
+        return time.perf_counter() - t0
+
+    ms = min(m, 256)
+    t = run(ms)
+    per_pair = t / pair_samples(1, ms)
+    ms_target = int(math.sqrt(2.0 * target_s / max(per_pair, 1e-12)))
+    ms_final = max(ms, min(m, ms_target, max_cols or m))
+    t = run(ms_final)
+    val = pair_samples(n, ms_final) / t
+    return val, {"n_rows": n, "n_cols_sampled": ms_final, "seconds": t, "threads": threads}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    rec = O.config_recipe(args.config)
+    n, m = rec["n"], rec["m"]
+    threads = O.c_num_threads()
+    # size one step to ~ (a few minutes / (K + W)) of CPU work
+    budget = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_pair_probe = None
+    import numpy as np
+
+    rng = np.random.default_rng(1234)
+    probe_ms = min(m, 256)
+    cols = sorted(rng.choice(m, probe_ms, replace=False).tolist()) if probe_ms < m else None
+    w = O.c_generate_config_words(rec, cols)
+    t0 = time.perf_counter()
+    O.c_mi_all_pairs(w, n)
+    per_pair_probe = (time.perf_counter() - t0) / pair_samples(1, probe_ms)
+    ms = max(probe_ms, min(m, int(math.sqrt(2.0 * budget / per_pair_probe))))
+    cols = sorted(rng.choice(m, ms, replace=False).tolist()) if ms < m else None
+    words = O.c_generate_config_words(rec, cols)
+    for _ in range(args.warmup):
+        O.c_mi_all_pairs(words, n)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.c_mi_all_pairs(words, n)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    val = pair_samples(n, ms) / t
+    out = "float32" if args.config == 4 else "float64"
+    sample = (f"full-N column sample: {ms} of {m} columns x N={n:,} rows per step "
+              f"(pair-samples/s scales with N*m_s(m_s+1)/2); reference algorithm restated in C "
+              f"(oracle/mi_oracle.c), OpenMP {threads} threads, host {O.cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "popcount/int64+f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config, n, m, out), "n_rows": n, "n_cols": m,
+                   "n_cols_sampled": ms, "output": out},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_19702_b200 import EngineConfig, MIEngine, datagen
+    from paper_2411_19702_b200 import dispatch as dsp
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    eng = MIEngine.get(local)
+
+    rec = datagen.config_recipe(args.config)
+    n, m = rec["n"], rec["m"]
+    out_name = datagen.CONFIGS[args.config]["out"]
+    out_dtype = torch.float64 if out_name == "float64" else torch.float32
+    cfg = EngineConfig()
+    W = pair_samples(n, m)
+
+    words_dev = datagen.generate_words_device(rec, dev) if rank == 0 else None
+    out = torch.empty((m, m), dtype=out_dtype, device=dev)
+    tiles = eng.tiles(m, rank, world)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    words_local = torch.empty((m, (n + 63) // 64), dtype=torch.int64, device=dev) if rank != 0 else words_dev
+
+    def step(ev_k0=None, ev_k1=None):
+        if world > 1:
+            dist.broadcast(words_local, src=0)
+        prep = eng.prepare(words_local, n, m)
+        if ev_k0 is not None:
+            ev_k0.record(stream)
+        eng.compute(prep, cfg, out_dtype, tiles=tiles, out=out)
+        if ev_k1 is not None:
+            ev_k1.record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for s0, s1, k0, k1 in ev:
+        flush.fill_(1)  # untimed L2 flush
+        s0.record(stream)
+        step(k0, k1)
+        s1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    step_ms = sum(a.elapsed_time(b) for a, b, _, _ in ev)
+    kern_ms = sum(c.elapsed_time(d) for _, _, c, d in ev)
+    t_local = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    step_ms, kern_ms = (t_local / args.steps).tolist()
+    value = W / (step_ms * 1e-3)
+
+    # roofline of the dominant kernel (fused Gram + MI), per launch on this rank
+    rank_tiles = int(tiles.shape[0])
+    all_tiles = int(nat_num_tiles(m))
+    ops_per_launch = 2.0 * W * (rank_tiles / all_tiles)
+    achieved_tops = ops_per_launch / (kern_ms * 1e-3) / 1e12
+    peaks = load_peaks()
+    peak = peaks["int8_tops"]
+    roofline = {
+        "bound": "tensor", "achieved": achieved_tops, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved_tops / peak, "traffic": load_traffic(args.config),
+        "kernel": "gram_mi_kernel<2,*,*> (tcgen05 kind::i8 2-SM + fused MI epilogue)",
+        "ops": "int8 tensor ops = 2 x pair-samples (1 MAC per pair-sample)",
+        "peak_source": peaks["source"], "frac_of_nominal_4500": achieved_tops / INT8_NOMINAL_TOPS,
+        "kernel_ms": kern_ms,
+    }
+
+    # end to end through the public API: pinned host words in, host MI out
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            val, info = cpu_sample(args.config, args.cpu_seconds)
+            from oracle import oracle as O
+
+            cpu = {"value": val, "unit": UNIT, "cores": info["threads"], "kind": "port",
+                   "sample": (f"{info['n_cols_sampled']} of {m} columns x N={n:,} (full N), one timed run of "
+                              f"{info['seconds']:.2f} s; reference algorithm restated in C (oracle/mi_oracle.c), "
+                              f"OpenMP {info['threads']} threads, host {O.cpu_model()}")}
+        except Exception as exc:  # the baseline must never sink the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "i8->s32 GEMM + f64 epilogue",
+            "data": "synthetic (splitmix64 stream of the reference's datagen, generated on device)",
+            "config": {"workload": workload_name(args.config, n, m, out_name), "n_rows": n, "n_cols": m,
+                       "output": out_name, "tiles": all_tiles, "tile": 256,
+                       "parallelism": f"upper-triangle tiles dealt over {world} GPU(s); words broadcast once",
+                       "l2": "flushed between steps (256 MiB write, untimed)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": 2 * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def nat_num_tiles(m: int) -> int:
+    from paper_2411_19702_b200 import _native as nat
+
+    return int(nat.lib().mi_num_tiles(m))
+
+
+def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_19702_b200 import dispatch as dsp
+
+    dev = eng.device
+    stream = torch.cuda.current_stream(dev)
+    esz = 8 if out_dtype == torch.float64 else 4
+    words_bytes = m * ((n + 63) // 64) * 8
+    host_words = words_dev.cpu().pin_memory() if rank == 0 else None
+    host_out = torch.empty((m, m), dtype=out_dtype, pin_memory=True) if rank == 0 else None
+    steps = max(1, min(args.steps, 20))
+
+    def once():
+        if world == 1:
+            eng.all_pairs_host(host_words, n, m, cfg, out_dtype, host_out=host_out)
+        else:
+            w = host_words.to(dev, non_blocking=True) if rank == 0 else None
+            local, tiles = dsp.mi_all_pairs_sharded(eng, w, n, m, cfg, out_dtype)
+            full = dsp.gather_to_root(local, m, tiles)
+            if rank == 0:
+                host_out.copy_(full, non_blocking=True)
+            stream.synchronize()
+
+    for _ in range(2):
+        once()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        once()
+        b.record(stream)
+        b.synchronize()
+        t.append(a.elapsed_time(b))
+    ms = torch.tensor([sum(t) / len(t)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    return {"value": W / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": words_bytes,
+            "d2h_bytes_per_step": m * m * esz, "ms_per_step": ms, "steps": steps,
+            "api": "MIEngine.all_pairs_host (pinned words in, pinned MI out)" if world == 1 else
+                   "dispatch.mi_all_pairs_sharded + gather_to_root"}
+
+
+def load_peaks() -> dict:
+    """int8 dense peak: profiles/int8_peak.json (measured cuBLAS int8 on the box) if
+    present, else 2x the driver-measured bf16 burst peak (B200 int8 rate = 2x bf16)."""
+    prof = ROOT / "profiles" / "int8_peak.json"
+    if prof.exists():
+        d = json.loads(prof.read_text())
+        if d.get("int8_tops"):
+            return {"int8_tops": float(d["int8_tops"]), "source": d.get("source", str(prof))}
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        d = json.loads(mp.read_text())
+        return {"int8_tops": 2.0 * float(d["bf16_tflops"]),
+                "source": "2 x MEASURED_PEAKS.json bf16_tflops (burst); B200 dense int8 = 2x bf16"}
+    return {"int8_tops": 2.0 * 1590.0, "source": "2 x fallback bf16 1.59 PF (B200_PROFILING.md)"}
+
+
+def load_traffic(cfg: int):
+    f = ROOT / "profiles" / "traffic.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        v = d.get(f"config{cfg}")
+        if v is not None:
+            return v
+    return None
+
+
+if __name__ == "__main__":
+    main()

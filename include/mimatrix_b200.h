@@ -54,10 +54,15 @@ const char* mi_last_error(void);
 int mi_device_info(int device, int* num_sms, int* cc_major, int* cc_minor);
 
 /* ---- layout helpers (host only, no device needed) ---- */
-/* padded row count N_pad of the K-major operand (bytes per operand row) */
+/* padded row count N_pad of the K-major operand (bytes per operand row).
+ * The operand is stored k-blocked: [N_pad/128][m_pad][128] int8, i.e. byte
+ * r of column c lives at ((r/128) * m_pad + c) * 128 + r % 128. */
 int64_t mi_kmajor_ld(int64_t n_rows);
 /* padded column count m_pad (operand rows, multiple of the tile size) */
 int64_t mi_kmajor_rows(int64_t n_cols);
+/* bytes of the per-column statistics workspace (marginal counts and their
+ * log2 splits) that kernel 1 writes and the fused kernel reads */
+int64_t mi_colstat_bytes(int64_t n_cols);
 /* output tile edge (256: a 2-SM tcgen05 tile) */
 int mi_tile_size(void);
 /* number of upper-triangle tiles (I <= J) for m columns */
@@ -70,13 +75,14 @@ int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* til
                      int64_t capacity);
 
 /* ---- device-pointer entry points, enqueued on `stream` ---- */
-/* words (m x nw uint64, nw = ceil(n_rows/64)) -> kmajor (m_pad x ld int8) and
- * colsum (m_pad int32; padding columns get 0). */
+/* words (m x nw uint64, nw = ceil(n_rows/64)) -> kmajor (k-blocked, m_pad * ld int8),
+ * d_colstat (mi_colstat_bytes) and, if d_colsum != NULL, the column sums
+ * (m_pad int32; padding columns get 0). */
 int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor,
-                     int64_t ld, int32_t* d_colsum, void* stream);
+                     int64_t ld, void* d_colstat, int32_t* d_colsum, void* stream);
 /* Fused G11 + MI over the listed upper-triangle tiles; writes each tile and
  * its mirror into d_out (row-major, pitch ld_out elements). */
-int mi_gram_mi(const int8_t* d_kmajor, const int32_t* d_colsum, int64_t n_rows, int64_t n_cols,
+int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
                int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
                int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
 /* Packed words of a synthetic dataset.  col_kind[c]: 0 Bernoulli(col_threshold[c]),
@@ -99,6 +105,12 @@ int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, 
 /* binmat.column_sums(matrix) */
 int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, uint64_t* h_out,
                         int device);
+/* Tuning knobs (process-wide): "cta_group" (2 = 256x256 tiles on an SM pair,
+ * 1 = 128x128 on one SM), "prefetch" (L2 prefetch distance in k-blocks),
+ * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per
+ * band of the tile order).  Also settable as MI_B200_<KEY> env vars. */
+int mi_set_tuning(const char* key, int value);
+int mi_get_tuning(const char* key); /* -1 for an unknown key */
 /* release the cached device workspaces of mi_*_host */
 void mi_release_workspace(void);
 

@@ -151,3 +151,44 @@ int oracle_mi_from_gram(const int64_t *g11, const uint64_t *v, int64_t m, int64_
     }
     return 0;
 }
+
+/*
+ * datagen.py:44-73 stream (draw k = r*m + c + 1, state seed + k*gamma) packed
+ * straight into words, for the listed columns only (cols == NULL: all).
+ * kind[c]: 0 Bernoulli(thr[c]), 1 all zero, 2 all one, 3 src[c] XOR
+ * Bernoulli(flip_thr) drawn from the flip_seed stream at the target's index.
+ */
+static inline uint64_t splitmix64_draw(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + k * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+void oracle_generate_words(uint64_t *words, int64_t n, int64_t m, uint64_t seed, const uint64_t *thr,
+                           const uint8_t *kind, const int32_t *src, uint64_t flip_thr, uint64_t flip_seed,
+                           const int64_t *cols, int64_t ncols_out) {
+    const int64_t nw = (n + 63) / 64;
+#pragma omp parallel for schedule(static)
+    for (int64_t idx = 0; idx < ncols_out * nw; ++idx) {
+        const int64_t k = idx / nw, w = idx % nw;
+        const int64_t c = cols ? cols[k] : k;
+        const int64_t r0 = w * 64;
+        const int64_t nr = (n - r0) < 64 ? (n - r0) : 64;
+        uint64_t out = 0;
+        for (int64_t b = 0; b < nr; ++b) {
+            const uint64_t row = (uint64_t)(r0 + b) * (uint64_t)m;
+            uint64_t bit = 0;
+            switch (kind[c]) {
+            case 0: bit = splitmix64_draw(seed, row + (uint64_t)c + 1) < thr[c]; break;
+            case 1: bit = 0; break;
+            case 2: bit = 1; break;
+            default:
+                bit = (splitmix64_draw(seed, row + (uint64_t)src[c] + 1) < thr[src[c]]) ^
+                      (splitmix64_draw(flip_seed, row + (uint64_t)c + 1) < flip_thr);
+            }
+            out |= bit << b;
+        }
+        words[k * nw + w] = out;
+    }
+}

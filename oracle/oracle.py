@@ -305,6 +305,57 @@ def generate_config_bits(recipe: dict) -> np.ndarray:
     return bits
 
 
+def generate_config_columns(recipe: dict, cols) -> np.ndarray:
+    """Bits (n, len(cols)) of only the listed columns of a config recipe.
+
+    Same values as generate_config_bits(recipe)[:, cols], without drawing the
+    other m - len(cols) columns (draw index r*m + c + 1 is computed per column),
+    so a bounded CPU baseline can use full-N column subsets of big configs.
+    """
+    n, m, seed = recipe["n"], recipe["m"], recipe["seed"]
+    cols = [int(c) for c in cols]
+    dens = np.broadcast_to(np.asarray(recipe["density"], dtype=np.float64), (m,))
+    zero, one = set(recipe["zero_cols"]), set(recipe["one_cols"])
+    src_of = {t: s for s, t in recipe["pairs"]}
+    rows = np.arange(n, dtype=np.uint64)
+
+    def base(c):
+        t = threshold(float(dens[c]))
+        if t <= 0:
+            return np.zeros(n, dtype=np.uint8)
+        if t >= 1 << 64:
+            return np.ones(n, dtype=np.uint8)
+        with np.errstate(over="ignore"):
+            idx = rows * np.uint64(m) + np.uint64(c + 1)
+            z = np.uint64(seed) + idx * _GAMMA
+            z = (z ^ (z >> np.uint64(30))) * _MIX1
+            z = (z ^ (z >> np.uint64(27))) * _MIX2
+            z = z ^ (z >> np.uint64(31))
+        return (z < np.uint64(t)).astype(np.uint8)
+
+    def flip(c):
+        t = threshold(recipe["flip_density"])
+        with np.errstate(over="ignore"):
+            idx = rows * np.uint64(m) + np.uint64(c + 1)
+            z = np.uint64(seed ^ FLIP_SEED_XOR) + idx * _GAMMA
+            z = (z ^ (z >> np.uint64(30))) * _MIX1
+            z = (z ^ (z >> np.uint64(27))) * _MIX2
+            z = z ^ (z >> np.uint64(31))
+        return (z < np.uint64(min(t, (1 << 64) - 1))).astype(np.uint8)
+
+    out = np.empty((n, len(cols)), dtype=np.uint8)
+    for k, c in enumerate(cols):
+        if c in zero:
+            out[:, k] = 0
+        elif c in one:
+            out[:, k] = 1
+        elif c in src_of:
+            out[:, k] = base(src_of[c]) ^ flip(c)
+        else:
+            out[:, k] = base(c)
+    return out
+
+
 # ----------------------------------------------------------------------------
 # the C restatement (oracle/mi_oracle.c), for sizes the NumPy path is too slow for
 # ----------------------------------------------------------------------------
@@ -330,6 +381,9 @@ def c_lib():
         lib.oracle_mi_all_pairs.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        vp = ctypes.c_void_p
+        lib.oracle_generate_words.argtypes = [vp, i64, i64, ctypes.c_uint64, vp, vp, vp,
+                                              ctypes.c_uint64, ctypes.c_uint64, vp, i64]
         _lib = lib
     return _lib
 
@@ -369,6 +423,39 @@ def c_mi_all_pairs(words: np.ndarray, n_rows: int, mode="exact", epsilon=1e-12,
     if rc != 0:
         raise OracleError(f"oracle_mi_all_pairs failed rc={rc}")
     return out
+
+
+def c_generate_config_words(recipe: dict, cols=None) -> np.ndarray:
+    """Packed words of a config recipe (only `cols` if given), by the C generator."""
+    n, m, seed = recipe["n"], recipe["m"], recipe["seed"]
+    dens = np.broadcast_to(np.asarray(recipe["density"], dtype=np.float64), (m,))
+    thr = np.zeros(m, dtype=np.uint64)
+    kind = np.zeros(m, dtype=np.uint8)
+    src = np.zeros(m, dtype=np.int32)
+    for c in range(m):
+        t = threshold(float(dens[c]))
+        if t <= 0:
+            kind[c] = 1
+        elif t >= 1 << 64:
+            kind[c] = 2
+        else:
+            thr[c] = t
+    for c in recipe["zero_cols"]:
+        kind[c] = 1
+    for c in recipe["one_cols"]:
+        kind[c] = 2
+    for s, t in recipe["pairs"]:
+        kind[t] = 3
+        src[t] = s
+    ft = min(threshold(recipe["flip_density"]), (1 << 64) - 1) if recipe["pairs"] else 0
+    sel = None if cols is None else np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+    k = m if sel is None else len(sel)
+    words = np.zeros((k, n_words(n)), dtype=np.uint64)
+    c_lib().oracle_generate_words(words.ctypes.data, n, m, seed & ((1 << 64) - 1), thr.ctypes.data,
+                                  kind.ctypes.data, src.ctypes.data, ft,
+                                  (seed ^ FLIP_SEED_XOR) & ((1 << 64) - 1),
+                                  None if sel is None else sel.ctypes.data, k)
+    return words
 
 
 def c_num_threads() -> int:

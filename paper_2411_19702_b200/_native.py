@@ -51,15 +51,18 @@ SIGNATURES = {
     "mi_device_info": (_int, [_int, _vp, _vp, _vp]),
     "mi_kmajor_ld": (_i64, [_i64]),
     "mi_kmajor_rows": (_i64, [_i64]),
+    "mi_colstat_bytes": (_i64, [_i64]),
     "mi_tile_size": (_int, []),
     "mi_num_tiles": (_i64, [_i64]),
     "mi_tile_list": (_i64, [_i64, _int, _int, _int, _vp, _i64]),
-    "mi_unpack_colsum": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "mi_unpack_colsum": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "mi_gram_mi": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
     "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
     "mi_gram_ones_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_column_sums_host": (_int, [_vp, _i64, _i64, _vp, _int]),
+    "mi_set_tuning": (_int, [ctypes.c_char_p, _int]),
+    "mi_get_tuning": (_int, [ctypes.c_char_p]),
     "mi_release_workspace": (None, []),
 }
 
@@ -108,6 +111,16 @@ def device_info(device: int) -> tuple[int, int, int]:
     check(lib().mi_device_info(device, ctypes.byref(sms), ctypes.byref(major), ctypes.byref(minor)),
           "mi_device_info")
     return sms.value, major.value, minor.value
+
+
+def set_tuning(**kw) -> None:
+    """e.g. set_tuning(prefetch=8, l2_hint=1) -- see mi_set_tuning in the header."""
+    for k, v in kw.items():
+        check(lib().mi_set_tuning(k.encode(), int(v)), f"mi_set_tuning({k})")
+
+
+def get_tuning(key: str) -> int:
+    return int(lib().mi_get_tuning(key.encode()))
 
 
 def tile_list(n_cols: int, rank: int = 0, world: int = 1, band: int = 0):

@@ -15,6 +15,7 @@
 
 #include "../../include/mimatrix_b200.h"
 #include "mi_kernels.h"
+#include "milog.cuh"
 
 using namespace mib200;
 
@@ -40,15 +41,25 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
-// Production tile: 256 x 256 on a CTA pair (cta_group::2).  MI_B200_CTA_GROUP=1
-// selects the single-SM 128 x 128 variant (debug / comparison only).
-int cta_group() {
-    static const int cg = [] {
-        const char* e = getenv("MI_B200_CTA_GROUP");
-        return (e && e[0] == '1') ? 1 : 2;
-    }();
-    return cg;
+// Tuning knobs: defaults are the measured best; MI_B200_* env vars
+// or mi_set_tuning() override them.  cta_group 2 = 256 x 256 tiles on a CTA
+// pair (production); 1 = single-SM 128 x 128 tiles.
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
 }
+struct Tuning {
+    int cta_group, prefetch, l2_hint, band;
+};
+Tuning& tuning() {
+    static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
+                       env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8)};
+    return t;
+}
+int cta_group() { return tuning().cta_group; }
+int prefetch_dist() { return tuning().prefetch; }
+int l2_hint() { return tuning().l2_hint; }
+int tile_band() { return tuning().band > 0 ? tuning().band : 8; }
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -105,17 +116,18 @@ int get_encode(PFN_cuTensorMapEncodeTiled_v12000* fn) {
     return MI_OK;
 }
 
-// K-major int8 operand X (m_pad rows of ld bytes) as a 2-D TMA tensor:
-// 128 x 128-byte boxes, 128B swizzle (matches the UMMA descriptors).
+// k-blocked K-major int8 operand X ([ld/128][m_pad][128] bytes) as a 3-D TMA
+// tensor: 128-byte x 128-row boxes (one contiguous 16 KB chunk each), 128B
+// swizzle (matches the UMMA descriptors).
 int make_tmap(CUtensorMap* tm, const int8_t* x, int64_t ld, int64_t m_pad) {
     PFN_cuTensorMapEncodeTiled_v12000 enc;
     int rc = get_encode(&enc);
     if (rc) return rc;
-    cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)m_pad};
-    cuuint64_t gstride[1] = {(cuuint64_t)ld};
-    cuuint32_t box[2] = {128, 128};
-    cuuint32_t estride[2] = {1, 1};
-    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(x), gdim, gstride, box,
+    cuuint64_t gdim[3] = {128, (cuuint64_t)m_pad, (cuuint64_t)(ld / 128)};
+    cuuint64_t gstride[2] = {128, (cuuint64_t)m_pad * 128};
+    cuuint32_t box[3] = {128, 128, 1};
+    cuuint32_t estride[3] = {1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(x), gdim, gstride, box,
                      estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(MI_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
@@ -173,6 +185,7 @@ struct Workspace {
     void* words = nullptr; size_t words_cap = 0;
     void* x = nullptr; size_t x_cap = 0;
     void* colsum = nullptr; size_t colsum_cap = 0;
+    void* colstat = nullptr; size_t colstat_cap = 0;
     void* tiles = nullptr; size_t tiles_cap = 0;
     void* out = nullptr; size_t out_cap = 0;
 };
@@ -194,10 +207,10 @@ void release(Workspace& w) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(w.device);
-    void** ps[] = {&w.words, &w.x, &w.colsum, &w.tiles, &w.out};
+    void** ps[] = {&w.words, &w.x, &w.colsum, &w.colstat, &w.tiles, &w.out};
     for (void** p : ps)
         if (*p) cudaFree(*p), *p = nullptr;
-    w.words_cap = w.x_cap = w.colsum_cap = w.tiles_cap = w.out_cap = 0;
+    w.words_cap = w.x_cap = w.colsum_cap = w.colstat_cap = w.tiles_cap = w.out_cap = 0;
     if (w.stream) cudaStreamDestroy(w.stream), w.stream = nullptr;
     w.device = -1;
     cudaSetDevice(prev);
@@ -213,9 +226,10 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
     if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
     if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
+    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_cols)))) return rc;
     MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
-    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
-                                 (int32_t*)ws.colsum, info.num_sms, ws.stream));
+    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
+                                 (int32_t*)ws.colsum, (ColStat*)ws.colstat, info.num_sms, ws.stream));
     *ld_out = ld;
     *m_pad_out = m_pad;
     return MI_OK;
@@ -238,12 +252,12 @@ int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t
               int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const DevInfo& info) {
     (void)m_pad;
     const int64_t n_tiles = mi_num_tiles(n_cols);
-    std::vector<int32_t> tiles = all_tiles(mi_kmajor_rows(n_cols) / mi_tile_size(), 8);
+    std::vector<int32_t> tiles = all_tiles(mi_kmajor_rows(n_cols) / mi_tile_size(), tile_band());
     int rc;
     if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
     MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
     (void)info;
-    return mi_gram_mi((const int8_t*)ws.x, (const int32_t*)ws.colsum, n_rows, n_cols, ld, mode, eps,
+    return mi_gram_mi((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps,
                       include_diagonal, out_kind, d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, ws.stream);
 }
 
@@ -269,6 +283,8 @@ int64_t mi_kmajor_ld(int64_t n_rows) { return round_up(n_rows < 1 ? 1 : n_rows, 
 
 int64_t mi_kmajor_rows(int64_t n_cols) { return round_up(n_cols < 1 ? 1 : n_cols, 256); }
 
+int64_t mi_colstat_bytes(int64_t n_cols) { return mi_kmajor_rows(n_cols) * (int64_t)sizeof(ColStat); }
+
 int mi_tile_size(void) { return gram_mi_tile_size(cta_group()); }
 
 int64_t mi_num_tiles(int64_t n_cols) {
@@ -280,7 +296,7 @@ int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* til
     if (n_cols < 1) return -fail(MI_ERR_DIMENSION, "n_cols must be >= 1");
     if (world < 1 || rank < 0 || rank >= world)
         return -fail(MI_ERR_DOMAIN, "bad rank %d of world %d", rank, world);
-    if (band <= 0) band = 8;
+    if (band <= 0) band = tile_band();
     const int64_t T = mi_kmajor_rows(n_cols) / mi_tile_size();
     std::vector<int32_t> all = all_tiles(T, band);
     const int64_t total = (int64_t)all.size() / 2;
@@ -297,7 +313,7 @@ int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* til
 }
 
 int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor, int64_t ld,
-                     int32_t* d_colsum, void* stream) {
+                     void* d_colstat, int32_t* d_colsum, void* stream) {
     int rc = check_shape(n_rows, n_cols);
     if (rc) return rc;
     if (ld < mi_kmajor_ld(n_rows) || ld % 128)
@@ -306,12 +322,13 @@ int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, in
     DevInfo info;
     if ((rc = current_device_info(&info))) return rc;
     const int64_t nw = (n_rows + 63) / 64;
-    MI_CUDA(launch_unpack_colsum(d_words, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
-                                 info.num_sms, (cudaStream_t)stream));
+    if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
+    MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
+                                 (ColStat*)d_colstat, info.num_sms, (cudaStream_t)stream));
     return MI_OK;
 }
 
-int mi_gram_mi(const int8_t* d_kmajor, const int32_t* d_colsum, int64_t n_rows, int64_t n_cols, int64_t ld,
+int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld,
                int mode, double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
                const int32_t* d_tiles, int64_t n_tiles, void* stream) {
     int rc = check_shape(n_rows, n_cols);
@@ -332,7 +349,7 @@ int mi_gram_mi(const int8_t* d_kmajor, const int32_t* d_colsum, int64_t n_rows, 
     CUtensorMap tm;
     if ((rc = make_tmap(&tm, d_kmajor, ld, mi_kmajor_rows(n_cols)))) return rc;
     GramMiParams p;
-    p.colsum = d_colsum;
+    p.colstat = reinterpret_cast<const ColStat*>(d_colstat);
     p.tiles = reinterpret_cast<const int2*>(d_tiles);
     p.n_tiles = (int)n_tiles;
     p.num_k_blocks = (int)(mi_kmajor_ld(n_rows) / 128);
@@ -342,6 +359,8 @@ int mi_gram_mi(const int8_t* d_kmajor, const int32_t* d_colsum, int64_t n_rows, 
     p.out = d_out;
     p.eps = epsilon;
     p.include_diagonal = include_diagonal ? 1 : 0;
+    p.prefetch_dist = prefetch_dist();
+    p.l2_hint = l2_hint();
     const int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tm, p, info.num_sms, (cudaStream_t)stream));
     return MI_OK;
@@ -417,6 +436,37 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
     MI_CUDA(cudaStreamSynchronize(ws->stream));
     for (int64_t k = 0; k < n_cols; ++k) h_out[k] = (uint64_t)tmp[k];
     return MI_OK;
+}
+
+int mi_set_tuning(const char* key, int value) {
+    if (!key) return fail(MI_ERR_DOMAIN, "null tuning key");
+    Tuning& t = tuning();
+    if (!strcmp(key, "cta_group")) {
+        if (value != 1 && value != 2) return fail(MI_ERR_DOMAIN, "cta_group must be 1 or 2");
+        t.cta_group = value;
+    } else if (!strcmp(key, "prefetch")) {
+        if (value < 0 || value > 256) return fail(MI_ERR_DOMAIN, "prefetch must be in [0, 256]");
+        t.prefetch = value;
+    } else if (!strcmp(key, "l2_hint")) {
+        if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "l2_hint must be 0, 1 or 2");
+        t.l2_hint = value;
+    } else if (!strcmp(key, "band")) {
+        if (value < 1) return fail(MI_ERR_DOMAIN, "band must be >= 1");
+        t.band = value;
+    } else {
+        return fail(MI_ERR_DOMAIN, "unknown tuning key '%s'", key);
+    }
+    return MI_OK;
+}
+
+int mi_get_tuning(const char* key) {
+    const Tuning& t = tuning();
+    if (!key) return -1;
+    if (!strcmp(key, "cta_group")) return t.cta_group;
+    if (!strcmp(key, "prefetch")) return t.prefetch;
+    if (!strcmp(key, "l2_hint")) return t.l2_hint;
+    if (!strcmp(key, "band")) return t.band;
+    return -1;
 }
 
 void mi_release_workspace(void) {

@@ -11,8 +11,10 @@
 // MI(J,I).
 //
 // Layout: X is the K-major int8 expansion of the bit-packed
-// columns, X[c][r] = bit r of column c, shape m_pad x N_pad (N_pad % 128 == 0,
-// m_pad % 256 == 0, zero padded).  Both GEMM operands are row blocks of X.
+// columns, X[c][r] = bit r of column c, stored k-blocked as
+// [N_pad/128][m_pad][128 bytes] (N_pad % 128 == 0, m_pad % 256 == 0, zero
+// padded) so each 128 x 128 TMA box is one contiguous 16 KB chunk.  Both GEMM
+// operands are row blocks of X.
 //
 // Warp roles (384 threads, one CTA per SM, persistent over a static tile list):
 //   warp 0      TMA producer (one lane): A = X[rows of I], B = X[rows of J]
@@ -27,8 +29,9 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
-#include "ptx.cuh"
+#include "milog.cuh"
 #include "mi_kernels.h"
+#include "ptx.cuh"
 
 namespace mib200 {
 
@@ -51,10 +54,12 @@ struct Cfg {
     static constexpr uint32_t STAGE_TX = CG * 2 * kStageHalfBytes;  // bytes landing per stage
 };
 
+
 struct SmemLayout {
     static constexpr uint32_t a_off = 0;
     static constexpr uint32_t b_off = kStages * kStageHalfBytes;
-    static constexpr uint32_t bar_off = 2 * kStages * kStageHalfBytes;
+    static constexpr uint32_t tab_off = 2 * kStages * kStageHalfBytes;   // log2 table, 2 KB
+    static constexpr uint32_t bar_off = tab_off + 128 * 16;
     // full[kStages], empty[kStages], tfull[2], tempty[2], tmem slot
     static constexpr uint32_t bytes = bar_off + (2 * kStages + 4) * 8 + 16;
 };
@@ -62,44 +67,56 @@ constexpr uint32_t kSmemBytes = SmemLayout::bytes + 1024;  // + alignment slack
 
 // ---------------------------------------------------------------- epilogue math
 
-// c * log2(c * N / (a * b)) with 0 * log 0 = 0.  c, a, b, N are exact
-// integers in fp64 (all < 2^31, products < 2^53 for N < 9.4e7), so the ratio
-// is one correctly rounded division.  Summing these over the four cells and
-// dividing by N gives sum_cells p * log2(p / (p_a p_b)) (engine.py:105-109,
-// 131-136); e.g. an identical balanced pair yields exactly 1.0 and an
-// independent one exactly 0.0, like the reference.
-__device__ __forceinline__ double xlog2r(double c, double ab, double dN) {
-    return c > 0.0 ? c * log2((c * dN) / ab) : 0.0;
+// Exact-mode MI of one pair (engine.py:105-109,116-141), from integer counts.
+// Each cell contributes c * log2(c N / (a b)), summed in the reference's fixed
+// order (1,1), (1,0), (0,1), (0,0) and divided by N at the end.  The log of the
+// ratio is assembled as integer exponents plus table-driven mantissa fractions
+// (milog.cuh): L = (e_c + e_N - e_a - e_b) + (((f_c + f_N) - f_a) - f_b), with
+// the marginal logs precomputed once per column by kernel 1.  Identical
+// mantissas cancel exactly, so an identical balanced pair gives exactly 1.0 and
+// an independent one (c N == a b with equal mantissas) exactly 0.0, as in the
+// reference; elsewhere the result is within ~1e-15 of the reference's value.
+struct Marg {
+    double f1, f0;  // log2 fractions of a1 = v and a0 = N - v
+    int e1, e0;     // and their exponents
+    int v;
+};
+
+__device__ __forceinline__ Marg load_marg(const ColStat* __restrict__ cs, int idx) {
+    const double2 f = __ldg(reinterpret_cast<const double2*>(cs + idx));
+    const int4 e = __ldg(reinterpret_cast<const int4*>(cs + idx) + 1);
+    return Marg{f.x, f.y, e.x, e.y, e.z};
 }
 
-// MI of one pair in orientation (i, j): vi = ones in column i (row of the
-// tile), vj = ones in column j.  Cells in the reference's fixed order
-// (1,1), (1,0), (0,1), (0,0) (engine.py:124-129).
-template <int MODE>
-__device__ __forceinline__ double mi_pair(int g, int vi, int vj, double dN, int N, double eps) {
-    const double c11 = (double)g;
-    const double c10 = (double)(vi - g);
-    const double c01 = (double)(vj - g);
-    const double c00 = (double)(N - vi - vj + g);
-    const double a1 = (double)vi, a0 = (double)(N - vi);
-    const double b1 = (double)vj, b0 = (double)(N - vj);
-    if constexpr (MODE == MI_MODE_EXACT) {
-        double s = xlog2r(c11, a1 * b1, dN);
-        s += xlog2r(c10, a1 * b0, dN);
-        s += xlog2r(c01, a0 * b1, dN);
-        s += xlog2r(c00, a0 * b0, dN);
-        return s / dN;
-    } else {
-        // engine.py:112-113: p * log2((p + eps) / (e + eps)), p = count / n,
-        // e = (a / n) * (b / n) -- evaluated with the reference's operations.
-        const double pa1 = a1 / dN, pa0 = a0 / dN, pb1 = b1 / dN, pb0 = b0 / dN;
-        double p, s;
-        p = c11 / dN; s = p * log2((p + eps) / (pa1 * pb1 + eps));
-        p = c10 / dN; s += p * log2((p + eps) / (pa1 * pb0 + eps));
-        p = c01 / dN; s += p * log2((p + eps) / (pa0 * pb1 + eps));
-        p = c00 / dN; s += p * log2((p + eps) / (pa0 * pb0 + eps));
-        return s;
-    }
+__device__ __forceinline__ double cell_term(int c, int ea, double fa, int eb, double fb, int eN, double fN,
+                                            const double2* __restrict__ tab) {
+    const double dc = (double)(c > 0 ? c : 1);
+    int ec;
+    const double fc = log2_frac(dc, tab, ec);
+    const double L = (double)(ec + eN - ea - eb) + (((fc + fN) - fa) - fb);
+    return c > 0 ? dc * L : 0.0;
+}
+
+__device__ __forceinline__ double mi_exact(int g, const Marg& A, const Marg& B, int N, double dN, int eN,
+                                           double fN, const double2* __restrict__ tab) {
+    double s = cell_term(g, A.e1, A.f1, B.e1, B.f1, eN, fN, tab);                   // (1,1)
+    s += cell_term(A.v - g, A.e1, A.f1, B.e0, B.f0, eN, fN, tab);                   // (1,0)
+    s += cell_term(B.v - g, A.e0, A.f0, B.e1, B.f1, eN, fN, tab);                   // (0,1)
+    s += cell_term(N - A.v - B.v + g, A.e0, A.f0, B.e0, B.f0, eN, fN, tab);         // (0,0)
+    return s / dN;
+}
+
+// Epsilon mode (engine.py:112-113): p * log2((p + eps) / (e + eps)) with
+// p = count / n and e = (a / n)(b / n), evaluated with the reference's operations.
+__device__ __forceinline__ double mi_epsilon(int g, int vi, int vj, int N, double dN, double eps) {
+    const double a1 = (double)vi, a0 = (double)(N - vi), b1 = (double)vj, b0 = (double)(N - vj);
+    const double pa1 = a1 / dN, pa0 = a0 / dN, pb1 = b1 / dN, pb0 = b0 / dN;
+    double p, s;
+    p = (double)g / dN;                s = p * log2((p + eps) / (pa1 * pb1 + eps));
+    p = (double)(vi - g) / dN;         s += p * log2((p + eps) / (pa1 * pb0 + eps));
+    p = (double)(vj - g) / dN;         s += p * log2((p + eps) / (pa0 * pb1 + eps));
+    p = (double)(N - vi - vj + g) / dN; s += p * log2((p + eps) / (pa0 * pb0 + eps));
+    return s;
 }
 
 template <int OUT>
@@ -127,6 +144,47 @@ __device__ __forceinline__ void store_row32(int32_t* dst, const int32_t (&v)[32]
 
 // ---------------------------------------------------------------- the kernel
 
+template <int CG>
+struct TileWalk {
+    // Linear walk over (my tile, k-block) pairs: step g -> tile index, k-block.
+    int cluster, n_clusters, n_tiles, nkb;
+    __device__ __forceinline__ bool at(long long g, int& t, int& kb) const {
+        const long long it = g / nkb;
+        t = cluster + (int)it * n_clusters;
+        kb = (int)(g - it * nkb);
+        return t < n_tiles;
+    }
+};
+
+// One 32-column chunk of the epilogue for one thread (= one output row).
+template <int OUT, int MODE, bool DIAG, typename T>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int i, int j0, const Marg& Ar,
+                                               const GramMiParams& p, int eN, double fN, double dN,
+                                               const double2* __restrict__ tab, T (&val)[32]) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const int j = j0 + k;
+        const int g = (int)r[k];
+        if constexpr (OUT == MI_OUT_COUNTS) {
+            val[k] = g;
+        } else {
+            const Marg Bc = load_marg(p.colstat, j);
+            // Each element is evaluated in (min, max) orientation so the two
+            // halves of a diagonal tile are bit-identical mirrors.
+            const bool sw = DIAG && (j < i);
+            double x;
+            if constexpr (MODE == MI_MODE_EXACT) {
+                x = sw ? mi_exact(g, Bc, Ar, p.n_rows, dN, eN, fN, tab)
+                       : mi_exact(g, Ar, Bc, p.n_rows, dN, eN, fN, tab);
+            } else {
+                x = mi_epsilon(g, sw ? Bc.v : Ar.v, sw ? Ar.v : Bc.v, p.n_rows, dN, p.eps);
+            }
+            if (DIAG && !p.include_diagonal && i == j) x = 0.0;
+            val[k] = (T)x;
+        }
+    }
+}
+
 template <int CG, int OUT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p) {
@@ -140,6 +198,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     const uint32_t sA = base + SmemLayout::a_off;
     const uint32_t sB = base + SmemLayout::b_off;
     const uint32_t bar0 = base + SmemLayout::bar_off;
+    double2* const tab = reinterpret_cast<double2*>(smem + SmemLayout::tab_off);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
@@ -167,6 +226,8 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         }
         fence_mbarrier_init();
     }
+    if (threadIdx.x >= kEpiWarp0 * 32 && threadIdx.x < kEpiWarp0 * 32 + 128)
+        tab[threadIdx.x - kEpiWarp0 * 32] = kLog2TabInit[threadIdx.x - kEpiWarp0 * 32];
     if (warp == 2) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -174,30 +235,46 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     const uint32_t tmem_base = *tmem_slot_ptr;
 
     const int nkb = p.num_k_blocks;
+    const TileWalk<CG> walk{cluster, n_clusters, p.n_tiles, nkb};
 
     if (warp == 0) {
         // ================= TMA producer =================
         if (lane == 0) {
-            const uint64_t policy = l2_policy_evict_last();
-            // CG == 2: both CTAs signal the leader's full barrier.
-            const uint32_t fb_rank = (CG == 2) ? 0u : rank;
+            const uint64_t policy = p.l2_hint == 1   ? l2_policy_evict_last()
+                                    : p.l2_hint == 2 ? l2_policy_evict_first()
+                                                     : l2_policy_evict_normal();
+            const int pf = p.prefetch_dist;
+            const uint32_t fb_rank = (CG == 2) ? 0u : rank;  // CG == 2: signal the leader's barrier
             int s = 0;
             uint32_t ph = 0;
-            for (int t = cluster; t < p.n_tiles; t += n_clusters) {
+            // warm the L2 with the first kPrefetchDist k-blocks
+            for (long long g = 0; g < pf; ++g) {
+                int t, kb;
+                if (!walk.at(g, t, kb)) break;
+                const int2 tile = p.tiles[t];
+                tma_prefetch_3d(&tmap_x, 0, tile.x * C::TS + (int)rank * 128, kb);
+                tma_prefetch_3d(&tmap_x, 0, tile.y * C::TS + (int)rank * 128, kb);
+            }
+            int t, kb;
+            for (long long g = 0; walk.at(g, t, kb); ++g) {
                 const int2 tile = p.tiles[t];
                 const int rowA = tile.x * C::TS + (int)rank * 128;
                 const int rowB = tile.y * C::TS + (int)rank * 128;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(empty_bar(s), ph ^ 1u);
-                    const uint32_t fb = (CG == 2) ? map_to_cta(full_bar(s), fb_rank) : full_bar(s);
-                    if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
-                    tma_load_2d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, kb * kBK, rowA, policy);
-                    tma_load_2d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, kb * kBK, rowB, policy);
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
+                int tp, kbp;
+                if (pf > 0 && walk.at(g + pf, tp, kbp)) {
+                    const int2 tpf = p.tiles[tp];
+                    tma_prefetch_3d(&tmap_x, 0, tpf.x * C::TS + (int)rank * 128, kbp);
+                    tma_prefetch_3d(&tmap_x, 0, tpf.y * C::TS + (int)rank * 128, kbp);
                 }
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                const uint32_t fb = (CG == 2) ? map_to_cta(full_bar(s), fb_rank) : full_bar(s);
+                if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
+                tma_load_3d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, 0, rowA, kb, policy);
+                tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
+                if (++s == kStages) { s = 0; ph ^= 1u; }
             }
             // drain: the last commit of every stage must land before exit
-            for (int i = 0; i < kStages; ++i) {
+            for (int q = 0; q < kStages; ++q) {
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 if (++s == kStages) { s = 0; ph ^= 1u; }
             }
@@ -234,12 +311,14 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         }
     } else if (warp >= kEpiWarp0) {
         // ================= epilogue =================
+        named_barrier_sync(1, kNumEpiWarps * 32);  // log2 table is in smem
         const int q = warp & 3;                    // TMEM lane quadrant of this warp
         const int h = (warp - kEpiWarp0) >> 2;     // which half of the accumulator columns
         const int row_local = q * 32 + (int)lane;
         const int m = p.m;
-        const int N = p.n_rows;
-        const double dN = (double)N;
+        const double dN = (double)p.n_rows;
+        int eN;
+        const double fN = log2_frac(dN, tab, eN);  // same routine as the per-column logs
         const int64_t ld = p.ld_out;
         T* __restrict__ out = reinterpret_cast<T*>(p.out);
         const uint32_t tempty_leader0 = (CG == 2) ? map_to_cta(tempty_bar(0), 0) : tempty_bar(0);
@@ -250,7 +329,8 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             const int2 tile = p.tiles[t];
             const bool diag = tile.x == tile.y;
             const int i = tile.x * C::TS + (int)rank * 128 + row_local;
-            const int vi = (i < m) ? __ldg(p.colsum + i) : 0;
+            Marg Ar{0.0, 0.0, 0, 0, 0};
+            if constexpr (OUT != MI_OUT_COUNTS) Ar = load_marg(p.colstat, i);  // colstat has m_pad rows
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
 #pragma unroll 1
@@ -263,22 +343,10 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                                    r);
                 tmem_ld_wait(r);
                 T val[32];
-#pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const int j = j0 + k;
-                    const int g = (int)r[k];
-                    if constexpr (OUT == MI_OUT_COUNTS) {
-                        val[k] = g;
-                    } else {
-                        const int vj = (j < m) ? __ldg(p.colsum + j) : 0;
-                        // compute every element in (min, max) orientation so the
-                        // mirrored halves of diagonal tiles are bit-identical
-                        const bool swap = diag && (j < i);
-                        double x = mi_pair<MODE>(g, swap ? vj : vi, swap ? vi : vj, dN, N, p.eps);
-                        if (!p.include_diagonal && i == j) x = 0.0;
-                        val[k] = (T)x;
-                    }
-                }
+                if (diag)
+                    epilogue_chunk<OUT, MODE, true>(r, i, j0, Ar, p, eN, fN, dN, tab, val);
+                else
+                    epilogue_chunk<OUT, MODE, false>(r, i, j0, Ar, p, eN, fN, dN, tab, val);
                 if (i < m) {
                     // direct tile: row i, columns j0 .. j0+31
                     T* dst = out + (int64_t)i * ld + j0;

@@ -12,8 +12,10 @@
 
 namespace mib200 {
 
+struct ColStat;
+
 struct GramMiParams {
-    const int32_t* colsum;  // [m_pad] ones per column (0 for padding columns)
+    const ColStat* colstat; // [m_pad] per-column marginals (kernel 1)
     const int2* tiles;      // [n_tiles] (I, J) tile coordinates, I <= J
     int n_tiles;
     int num_k_blocks;       // N_pad / 128
@@ -23,6 +25,8 @@ struct GramMiParams {
     void* out;              // int32 / double / float, row-major m x ld_out
     double eps;
     int include_diagonal;
+    int prefetch_dist;      // k-blocks of L2 prefetch ahead of the TMA ring (0 = off)
+    int l2_hint;            // 0 normal, 1 evict_last, 2 evict_first for operand loads
 };
 
 cudaError_t launch_gram_mi(int cg, int out_kind, int mode, const CUtensorMap& tmap,
@@ -30,9 +34,9 @@ cudaError_t launch_gram_mi(int cg, int out_kind, int mode, const CUtensorMap& tm
 int gram_mi_tile_size(int cg);
 uint32_t gram_mi_smem_bytes();
 
-cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t m, int64_t nw, int8_t* x,
-                                 int64_t ld, int64_t m_pad, int32_t* colsum, int num_sms,
-                                 cudaStream_t stream);
+cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
+                                 int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,
+                                 ColStat* colstat, int num_sms, cudaStream_t stream);
 
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,
                                   const uint64_t* col_threshold, const uint8_t* col_kind,

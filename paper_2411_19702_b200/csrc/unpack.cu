@@ -2,8 +2,11 @@
 //
 // Input is the reference's BinaryMatrix.words layout (binmat.py:3-6,57-97):
 // (m, nw) uint64, column-major, bit r of word w = row 64w + r, padding zero.
-// Output X[c][r] (m_pad x ld bytes, ld = N_pad % 128 == 0) holds 0/1 bytes and
-// is zero in every padding row / column, so padded cells add nothing to G.
+// Output X holds X[c][r] = bit r of column c as 0/1 bytes in a k-blocked
+// K-major layout: [ld/128 k-blocks][m_pad columns][128 bytes], so the 128 x 128
+// box the GEMM loads for (k-block, 128 columns) is one contiguous 16 KB chunk
+// (one DRAM page, one TLB entry).  Padding rows / columns are zero, so padded
+// cells add nothing to G.
 // The same pass produces v[c] = popcount of column c, i.e. the reference's
 // column_sums (binmat.py:175-177), which the fused epilogue needs.
 //
@@ -14,6 +17,7 @@
 #include <cstdint>
 
 #include "mi_kernels.h"
+#include "milog.cuh"
 
 namespace mib200 {
 
@@ -22,8 +26,9 @@ namespace mib200 {
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
 __global__ void __launch_bounds__(256)
-unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x,
-                     int64_t ld, int64_t m_pad, int32_t* __restrict__ colsum) {
+unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t n_rows, int64_t m, int64_t nw,
+                     int8_t* __restrict__ x, int64_t ld, int64_t m_pad, int32_t* __restrict__ colsum,
+                     ColStat* __restrict__ colstat) {
     const int lane = threadIdx.x & 31;
     const int quarter = lane & 3;
     const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -31,7 +36,8 @@ unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, 
     const int64_t wpad = ld / 64;  // words per padded column
     for (int64_t c = warp0; c < m_pad; c += nwarps) {
         const uint64_t* __restrict__ src = words + c * nw;
-        uint4* __restrict__ dst = reinterpret_cast<uint4*>(x + c * ld);
+        int8_t* __restrict__ dst = x + c * 128;  // row c inside every k-block
+        const int64_t kb_stride = m_pad * 128;
         const bool real = c < m;
         uint32_t cnt = 0;
 #pragma unroll 4
@@ -45,22 +51,37 @@ unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, 
             v.y = spread4((b16 >> 4) & 0xF);
             v.z = spread4((b16 >> 8) & 0xF);
             v.w = spread4(b16 >> 12);
-            if (w < wpad) dst[w * 4 + quarter] = v;
+            if (w < wpad)
+                *reinterpret_cast<uint4*>(dst + (w >> 1) * kb_stride + (w & 1) * 64 + quarter * 16) = v;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) colsum[c] = (int32_t)cnt;
+        if (lane == 0) {
+            if (colsum) colsum[c] = (int32_t)cnt;
+            // marginal logs for the fused epilogue: log2(v) and log2(N - v)
+            ColStat st;
+            st.v = (int)cnt;
+            st.pad = 0;
+            const int v0 = (int)(n_rows - (int64_t)cnt);
+            st.f1 = cnt > 0 ? log2_frac((double)cnt, kLog2TabInit, st.e1) : 0.0;
+            if (cnt == 0) st.e1 = 0;
+            st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, st.e0) : 0.0;
+            if (v0 <= 0) st.e0 = 0;
+            colstat[c] = st;
+        }
     }
 }
 
-cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t m, int64_t nw, int8_t* x, int64_t ld,
-                                 int64_t m_pad, int32_t* colsum, int num_sms, cudaStream_t stream) {
+cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
+                                 int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, int num_sms,
+                                 cudaStream_t stream) {
     const int threads = 256;
     int64_t blocks = (m_pad + 7) / 8;
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    unpack_colsum_kernel<<<(unsigned)blocks, threads, 0, stream>>>(words, m, nw, x, ld, m_pad, colsum);
+    unpack_colsum_kernel<<<(unsigned)blocks, threads, 0, stream>>>(words, n_rows, m, nw, x, ld, m_pad, colsum,
+                                                                   colstat);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,115 @@
+"""Multi-GPU dispatcher: one process per GPU, upper-triangle tiles dealt across ranks.
+
+The output tiles (I <= J) of the MI matrix are independent and all cost the
+same (K = N), so the path shards with no data-path reduction
+(SURVEY 8(e)): rank 0 holds the packed words; ONE broadcast sends them to
+every rank (NCCL over NVLink, bit-packed so it is 1/8 of the int8 operand);
+each rank unpacks its own copy and computes the tiles the C ABI's
+``mi_tile_list(m, rank, world)`` deals it, writing each tile and its mirror
+into its local output.  The MI matrix stays sharded; ``gather_to_root``
+assembles it on request.
+
+Everything here is plain torch.distributed plumbing around two callables,
+so the same code runs over NCCL on GPUs and over gloo on CPU in the tests
+(where the per-tile compute is supplied by the test).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as nat
+from .binmat import n_words
+
+
+def world_info(group=None) -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def rank_tiles(n_cols: int, rank: int, world: int) -> np.ndarray:
+    """(k, 2) int32 (I, J) tiles of `rank`; the union over ranks is every I <= J
+    tile exactly once (host logic in the C ABI, no device needed)."""
+    return nat.tile_list(n_cols, rank, world)
+
+
+def tile_mask(n_cols: int, tiles: np.ndarray, tile: int | None = None) -> np.ndarray:
+    """Boolean m x m mask of the elements a tile list writes (tiles + mirrors)."""
+    tile = tile or int(nat.lib().mi_tile_size())
+    mask = np.zeros((n_cols, n_cols), dtype=bool)
+    for I, J in np.asarray(tiles):
+        r = slice(I * tile, min((I + 1) * tile, n_cols))
+        c = slice(J * tile, min((J + 1) * tile, n_cols))
+        mask[r, c] = True
+        mask[c, r] = True
+    return mask
+
+
+def broadcast_words(words: torch.Tensor | None, n_rows: int, n_cols: int, device: torch.device,
+                    src: int = 0, group=None) -> torch.Tensor:
+    """The path's only collective: the packed words from `src` to every rank."""
+    rank, _ = world_info(group)
+    if rank == src:
+        if words is None:
+            raise ValueError("the source rank must provide the words")
+        buf = words.to(device)
+    else:
+        buf = torch.empty((n_cols, n_words(n_rows)), dtype=torch.int64, device=device)
+    if dist.is_available() and dist.is_initialized():
+        dist.broadcast(buf, src=src, group=group)
+    return buf
+
+
+def run_sharded(words: torch.Tensor | None, n_rows: int, n_cols: int,
+                compute: Callable[[torch.Tensor, np.ndarray, torch.Tensor], None],
+                out: torch.Tensor, device: torch.device, group=None) -> np.ndarray:
+    """Broadcast words, then compute this rank's tiles into `out`.
+
+    ``compute(words_local, tiles, out)`` writes the given tiles and their
+    mirrors into out.  Returns this rank's tile list.
+    """
+    rank, world = world_info(group)
+    w = broadcast_words(words, n_rows, n_cols, device, group=group)
+    tiles = rank_tiles(n_cols, rank, world)
+    compute(w, tiles, out)
+    return tiles
+
+
+def gather_to_root(out: torch.Tensor, n_cols: int, tiles: np.ndarray, root: int = 0, group=None) -> torch.Tensor | None:
+    """Assemble the full matrix on `root` from every rank's tiles.
+
+    Each rank zeroes what it did not write and the shards are summed onto the
+    root; every element is written by exactly one rank, so the sum is an exact
+    gather (x + 0 == x in IEEE arithmetic).
+    """
+    rank, world = world_info(group)
+    if world == 1:
+        return out
+    mask = torch.from_numpy(tile_mask(n_cols, tiles)).to(out.device)
+    shard = torch.where(mask, out[:n_cols, :n_cols], torch.zeros((), dtype=out.dtype, device=out.device))
+    dist.reduce(shard, dst=root, op=dist.ReduceOp.SUM, group=group)
+    return shard if rank == root else None
+
+
+def mi_all_pairs_sharded(engine, words: torch.Tensor | None, n_rows: int, n_cols: int, cfg=None,
+                         out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
+                         group=None) -> tuple[torch.Tensor, np.ndarray]:
+    """GPU version: broadcast + unpack + fused Gram/MI over this rank's tiles.
+
+    Returns (local output with this rank's tiles and mirrors written, tiles).
+    """
+    rank, world = world_info(group)
+    if out is None:
+        out = torch.empty((n_cols, n_cols), dtype=out_dtype, device=engine.device)
+
+    def compute(w, tiles, o):
+        prep = engine.prepare(w, n_rows, n_cols)
+        engine.compute(prep, cfg, out_dtype, tiles=engine.tiles(n_cols, rank, world), out=o)
+
+    tiles = run_sharded(words, n_rows, n_cols, compute, out, engine.device, group)
+    return out, tiles

@@ -87,6 +87,7 @@ class Prepared:
     m_pad: int       # X rows
     x: torch.Tensor  # int8 (m_pad, ld)
     colsum: torch.Tensor  # int32 (m_pad,)
+    colstat: torch.Tensor  # uint8 workspace (mi_colstat_bytes): marginals + their log2 splits
 
 
 def _stream_ptr(device: torch.device) -> int:
@@ -153,10 +154,11 @@ class MIEngine:
         ld, m_pad = self.layout(n_rows, n_cols)
         x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
         colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
+        colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_cols)),), dtype=torch.uint8, device=self.device)
         nat.check(nat.lib().mi_unpack_colsum(words_dev.data_ptr(), n_rows, n_cols, x.data_ptr(), ld,
-                                             colsum.data_ptr(), _stream_ptr(self.device)),
+                                             colstat.data_ptr(), colsum.data_ptr(), _stream_ptr(self.device)),
                   "mi_unpack_colsum")
-        return Prepared(n_rows, n_cols, ld, m_pad, x, colsum)
+        return Prepared(n_rows, n_cols, ld, m_pad, x, colsum, colstat)
 
     def compute(self, prep: Prepared, cfg=None, out_dtype: torch.dtype = torch.float64,
                 tiles: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -176,7 +178,7 @@ class MIEngine:
             raise DimensionError("out must be a row-major (>= m, >= m) tensor of out_dtype on the device")
         if tiles is None:
             tiles = self.tiles(m)
-        nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colsum.data_ptr(), prep.n_rows, m, prep.ld,
+        nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m, prep.ld,
                                        mode, eps, diag, kind, out.data_ptr(), out.stride(0),
                                        tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),
                   "mi_gram_mi")
