@@ -1,0 +1,182 @@
+"""Host-side logic and the C-ABI boundary, without a GPU.
+
+No compute calls: only loading the library, checking its exports, the pure
+host helpers (layout, tile lists) and argument validation that fails before
+any device work.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import rand_bits
+from oracle import oracle as O
+from paper_2411_19702_b200 import (
+    BACKENDS,
+    BinaryMatrix,
+    DimensionError,
+    DomainError,
+    EngineConfig,
+    NativeError,
+    from_bits,
+    from_rows,
+    mi_all_pairs,
+)
+from paper_2411_19702_b200 import _native as nat
+from paper_2411_19702_b200 import datagen, dispatch
+
+
+# ------------------------------------------------------------------ C ABI
+def test_library_exports_every_header_function():
+    lib = nat.lib()
+    declared = nat.header_functions()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/mimatrix_b200.h but not exported"
+    assert set(declared) == set(nat.SIGNATURES), "ctypes signatures out of sync with the header"
+    assert lib.mi_b200_abi_version() == 1
+
+
+def test_layout_helpers():
+    lib = nat.lib()
+    assert lib.mi_kmajor_ld(1) == 128 and lib.mi_kmajor_ld(128) == 128 and lib.mi_kmajor_ld(129) == 256
+    assert lib.mi_kmajor_rows(1) == 256 and lib.mi_kmajor_rows(257) == 512
+    assert lib.mi_tile_size() in (128, 256)
+    T = lib.mi_kmajor_rows(10000) // lib.mi_tile_size()
+    assert lib.mi_num_tiles(10000) == T * (T + 1) // 2
+    assert lib.mi_colstat_bytes(300) == 512 * 32
+
+
+@pytest.mark.parametrize("m", [1, 255, 256, 257, 1000, 10000, 50000])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_tile_partition_covers_triangle_once(m, world):
+    lib = nat.lib()
+    T = lib.mi_kmajor_rows(m) // lib.mi_tile_size()
+    seen = {}
+    counts = []
+    for r in range(world):
+        tl = nat.tile_list(m, r, world)
+        counts.append(len(tl))
+        for I, J in tl.tolist():
+            assert 0 <= I <= J < T
+            assert (I, J) not in seen, "tile dealt twice"
+            seen[(I, J)] = r
+    assert len(seen) == T * (T + 1) // 2
+    assert max(counts) - min(counts) <= 1, "unbalanced shares"
+
+
+def test_tile_mask_covers_matrix():
+    m = 600
+    full = np.zeros((m, m), dtype=int)
+    for r in range(3):
+        full += dispatch.tile_mask(m, nat.tile_list(m, r, 3))
+    assert np.all(full >= 1)
+    # an element is written by exactly one rank (tile + mirror of the same tile)
+    disjoint = np.zeros((m, m), dtype=int)
+    for r in range(3):
+        tl = nat.tile_list(m, r, 3)
+        t = nat.lib().mi_tile_size()
+        for I, J in tl.tolist():
+            disjoint[I * t:(I + 1) * t, J * t:(J + 1) * t] += 1
+    assert np.all(np.triu(disjoint[:m, :m]) <= 1)
+
+
+def test_c_abi_rejects_bad_arguments_without_device_work():
+    lib = nat.lib()
+    assert lib.mi_tile_list(100, 3, 2, 0, None, 0) < 0
+    assert lib.mi_tile_list(0, 0, 1, 0, None, 0) < 0
+    rc = lib.mi_gram_mi(None, None, 0, 10, 128, 0, 1e-12, 1, 1, None, 10, None, 1, None)
+    assert rc == nat.MI_ERR_DIMENSION
+    rc = lib.mi_gram_mi(None, None, 10, 10, 128, 7, 1e-12, 1, 1, None, 10, None, 1, None)
+    assert rc == nat.MI_ERR_DOMAIN and "mode" in nat.last_error()
+    rc = lib.mi_gram_mi(None, None, 10, 10, 128, 1, 0.0, 1, 1, None, 10, None, 1, None)
+    assert rc == nat.MI_ERR_DOMAIN
+    rc = lib.mi_gram_mi(None, None, 10, 10, 64, 0, 1e-12, 1, 1, None, 10, None, 1, None)
+    assert rc == nat.MI_ERR_DIMENSION
+    with pytest.raises(DomainError):
+        nat.check(nat.MI_ERR_DOMAIN, "x")
+    words = np.array([[0b111]], dtype=np.uint64)  # dirty padding for n_rows = 2
+    out = np.empty((1, 1))
+    rc = lib.mi_all_pairs_host(words.ctypes.data, 2, 1, 0, 1e-12, 1, 1, out.ctypes.data, 0)
+    assert rc == nat.MI_ERR_DOMAIN and "padding" in nat.last_error()
+
+
+def test_tuning_knobs_roundtrip():
+    old = nat.get_tuning("band")
+    nat.set_tuning(band=4)
+    assert nat.get_tuning("band") == 4
+    nat.set_tuning(band=old)
+    with pytest.raises(DomainError):
+        nat.set_tuning(cta_group=3)
+    with pytest.raises(DomainError):
+        nat.set_tuning(nonsense=1)
+
+
+# ------------------------------------------------------------------ data model
+def test_binary_matrix_validation():
+    """binmat.py:71-80 / test_binmat.py:101-104 semantics."""
+    with pytest.raises(DimensionError):
+        BinaryMatrix(0, 1, np.zeros((1, 0), dtype=np.uint64))
+    with pytest.raises(DimensionError):
+        BinaryMatrix(3, 2, np.zeros((2, 2), dtype=np.uint64))
+    with pytest.raises(DomainError):
+        BinaryMatrix(2, 1, np.array([[0b111]], dtype=np.uint64))
+    with pytest.raises(DimensionError):
+        from_rows([])
+    with pytest.raises(DimensionError):
+        from_rows([[1, 0], [1]])
+    with pytest.raises(DomainError):
+        from_rows([[0, 2]])
+    m = from_rows([[1, 0], [0, 1], [1, 1]])
+    assert m.words.tolist() == [[0b101], [0b110]]
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 128, 130])
+def test_pack_matches_oracle(n):
+    bits = rand_bits(np.random.default_rng(n), n, 5, 0.5)
+    assert np.array_equal(from_bits(bits).words, O.pack_bits(bits))
+    assert np.array_equal(from_bits(bits).to_bits(), bits)
+
+
+def test_engine_config_and_backend_validation():
+    with pytest.raises(DomainError):
+        EngineConfig(mode="fuzzy")
+    with pytest.raises(DomainError):
+        EngineConfig(mode="epsilon", epsilon=0.0)
+    assert BACKENDS == ("dense", "sparse", "direct")
+    mat = from_rows([[1]])
+    with pytest.raises(DomainError):
+        mi_all_pairs(mat, backend="gpu")  # test_engine.py:152-154
+
+
+def test_no_silent_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(NativeError):
+        mi_all_pairs(from_rows([[1, 0], [0, 1]]))
+
+
+# ------------------------------------------------------------------ datagen program
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_product_recipe_agrees_with_oracle(cfg):
+    n, m = {1: (1000, 500), 2: (3000, 600), 3: (100, 70), 4: (2000, 1000), 5: (400, 300)}[cfg]
+    a = datagen.config_recipe(cfg, n, m)
+    b = O.config_recipe(cfg, n, m)
+    assert np.array_equal(a["density"], b["density"])
+    assert a["zero_cols"] == b["zero_cols"] and a["one_cols"] == b["one_cols"]
+    assert [tuple(p) for p in a["pairs"]] == [tuple(p) for p in b["pairs"]]
+    thr, kind, src, ft = datagen.column_program(a)
+    assert ((kind == 3).sum()) == len(a["pairs"])
+    for c in a["zero_cols"]:
+        assert kind[c] == 1
+    assert datagen.threshold(0.5) == 1 << 63
+
+
+def test_signature_binding_types():
+    fn = nat.lib().mi_all_pairs_host
+    assert fn.restype is ctypes.c_int and len(fn.argtypes) == 9
