@@ -108,7 +108,8 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
 /* Tuning knobs (process-wide): "cta_group" (2 = 256x256 tiles on an SM pair,
  * 1 = 128x128 on one SM), "prefetch" (L2 prefetch distance in k-blocks),
  * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per
- * band of the tile order).  Also settable as MI_B200_<KEY> env vars. */
+ * band of the tile order), "stages" (smem ring depth), "epi_warps" (8 or 16
+ * epilogue warps).  Also settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key */
 /* release the cached device workspaces of mi_*_host */

@@ -49,11 +49,12 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
-                       env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8)};
+                       env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8),
+                       env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -362,7 +363,7 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
     p.prefetch_dist = prefetch_dist();
     p.l2_hint = l2_hint();
     const int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
-    MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tm, p, info.num_sms, (cudaStream_t)stream));
+    MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tuning().stages, tuning().epi_warps, tm, p, info.num_sms, (cudaStream_t)stream));
     return MI_OK;
 }
 
@@ -453,6 +454,12 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "band")) {
         if (value < 1) return fail(MI_ERR_DOMAIN, "band must be >= 1");
         t.band = value;
+    } else if (!strcmp(key, "stages")) {
+        if (value != 6) return fail(MI_ERR_DOMAIN, "stages must be 6");
+        t.stages = value;
+    } else if (!strcmp(key, "epi_warps")) {
+        if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");
+        t.epi_warps = value;
     } else {
         return fail(MI_ERR_DOMAIN, "unknown tuning key '%s'", key);
     }
@@ -466,6 +473,8 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "prefetch")) return t.prefetch;
     if (!strcmp(key, "l2_hint")) return t.l2_hint;
     if (!strcmp(key, "band")) return t.band;
+    if (!strcmp(key, "stages")) return t.stages;
+    if (!strcmp(key, "epi_warps")) return t.epi_warps;
     return -1;
 }
 

@@ -16,12 +16,10 @@
 // padded) so each 128 x 128 TMA box is one contiguous 16 KB chunk.  Both GEMM
 // operands are row blocks of X.
 //
-// Warp roles (384 threads, one CTA per SM, persistent over a static tile list):
-//   warp 0      TMA producer (one lane): A = X[rows of I], B = X[rows of J]
-//   warp 1      MMA issuer (one lane, leader CTA only when CG == 2)
-//   warp 2      TMEM allocator
-//   warp 3      idle
-//   warps 4-11  epilogue: tcgen05.ld -> counts -> fp64 MI -> global
+// Warp roles (one CTA per SM, persistent over a static tile list):
+//   warp 0            TMA producer (one lane): A = X[rows of I], B = X[rows of J]
+//   warp 1            TMEM allocator; then MMA issuer (one lane, leader CTA)
+//   warps 2 .. 2+E-1  epilogue (E = 8 or 16): tcgen05.ld -> counts -> MI -> global
 // CG == 2: a CTA pair (cluster of 2) computes a 256x256 tile with
 // tcgen05.mma.cta_group::2 (M=256, N=256); each CTA stages half of A and half
 // of B, and owns 128 accumulator rows.  CG == 1: 128x128 tiles on one SM.
@@ -35,87 +33,119 @@
 
 namespace mib200 {
 
-constexpr int kThreads = 384;
-constexpr int kEpiWarp0 = 4;
-constexpr int kNumEpiWarps = 8;
-constexpr int kBK = 128;                 // K bytes per pipeline stage (= 128B swizzle span)
+constexpr int kEpiWarp0 = 2;
+constexpr int kBK = 128;                    // K bytes per pipeline stage (= 128B swizzle span)
 constexpr int kStageHalfBytes = 128 * kBK;  // one 128-row operand half: 16 KB
-constexpr int kStages = 6;
+constexpr uint32_t kMaxSmem = 232448;       // 227 KB opt-in per CTA on sm_100
 
-template <int CG>
+template <int CG, int EW>
 struct Cfg {
-    static constexpr int TS = 128 * CG;           // square output tile
+    static constexpr int TS = 128 * CG;             // square output tile
     static constexpr int MMA_M = 128 * CG;
     static constexpr int MMA_N = 128 * CG;
-    static constexpr int ACC_COLS = MMA_N;        // TMEM columns per accumulator
+    static constexpr int ACC_COLS = MMA_N;          // TMEM columns per accumulator
     static constexpr int TMEM_COLS = 2 * ACC_COLS;  // double-buffered
-    static constexpr int HALF_COLS = ACC_COLS / 2;  // columns per epilogue warp
-    static constexpr int CHUNKS = HALF_COLS / 32;
+    static constexpr int EPI_WARPS = EW;
+    static constexpr int THREADS = 32 * (kEpiWarp0 + EW);
+    static constexpr int COL_PARTS = EW / 4;        // epilogue warps per TMEM lane quadrant
+    static constexpr int WARP_COLS = ACC_COLS / COL_PARTS;
     static constexpr uint32_t STAGE_TX = CG * 2 * kStageHalfBytes;  // bytes landing per stage
+    static_assert(EW % 4 == 0 && WARP_COLS % 16 == 0, "bad epilogue split");
 };
 
-
+template <int CG, int ST>
 struct SmemLayout {
     static constexpr uint32_t a_off = 0;
-    static constexpr uint32_t b_off = kStages * kStageHalfBytes;
-    static constexpr uint32_t tab_off = 2 * kStages * kStageHalfBytes;   // log2 table, 2 KB
-    static constexpr uint32_t bar_off = tab_off + 128 * 16;
-    // full[kStages], empty[kStages], tfull[2], tempty[2], tmem slot
-    static constexpr uint32_t bytes = bar_off + (2 * kStages + 4) * 8 + 16;
+    static constexpr uint32_t b_off = ST * kStageHalfBytes;
+    static constexpr uint32_t tab_off = 2 * ST * kStageHalfBytes;  // log2 table, 2 KB
+    static constexpr uint32_t col_off = tab_off + 128 * 16;        // column stats [2][TS]
+    static constexpr uint32_t bar_off = col_off + 2 * 128 * CG * (uint32_t)sizeof(ColStat);
+    // full[ST], empty[ST], tfull[2], tempty[2], tmem slot
+    static constexpr uint32_t bytes = bar_off + (2 * ST + 4) * 8 + 16;
+    // + alignment slack when it fits (the dynamic window is normally 1 KB aligned)
+    static constexpr uint32_t request = bytes + 1024 <= kMaxSmem ? bytes + 1024 : kMaxSmem;
+    static_assert(bytes <= kMaxSmem, "pipeline does not fit in shared memory");
 };
-constexpr uint32_t kSmemBytes = SmemLayout::bytes + 1024;  // + alignment slack
 
 // ---------------------------------------------------------------- epilogue math
-
+//
 // Exact-mode MI of one pair (engine.py:105-109,116-141), from integer counts.
 // Each cell contributes c * log2(c N / (a b)), summed in the reference's fixed
 // order (1,1), (1,0), (0,1), (0,0) and divided by N at the end.  The log of the
 // ratio is assembled as integer exponents plus table-driven mantissa fractions
-// (milog.cuh): L = (e_c + e_N - e_a - e_b) + (((f_c + f_N) - f_a) - f_b), with
-// the marginal logs precomputed once per column by kernel 1.  Identical
+// (milog.cuh): L = ((e_c + ((e_N - e_a) - e_b)) + (((f_c + f_N) - f_a) - f_b),
+// with the marginal logs precomputed once per column by kernel 1.  Identical
 // mantissas cancel exactly, so an identical balanced pair gives exactly 1.0 and
 // an independent one (c N == a b with equal mantissas) exactly 0.0, as in the
 // reference; elsewhere the result is within ~1e-15 of the reference's value.
-struct Marg {
-    double f1, f0;  // log2 fractions of a1 = v and a0 = N - v
-    int e1, e0;     // and their exponents
-    int v;
+// All counts are exact integers held in doubles; no I2F conversions.
+
+struct RowMarg {        // the tile row's (A side) marginals
+    double v, nv;       // v_i, N - v_i
+    double er1, er0;    // e_N - e(v_i), e_N - e(N - v_i)
+    double f1, f0;
 };
 
-__device__ __forceinline__ Marg load_marg(const ColStat* __restrict__ cs, int idx) {
-    const double2 f = __ldg(reinterpret_cast<const double2*>(cs + idx));
-    const int4 e = __ldg(reinterpret_cast<const int4*>(cs + idx) + 1);
-    return Marg{f.x, f.y, e.x, e.y, e.z};
+__device__ __forceinline__ RowMarg row_marg(const ColStat& s, double eN) {
+    return RowMarg{s.v, s.nv, eN - s.e1, eN - s.e0, s.f1, s.f0};
 }
 
-__device__ __forceinline__ double cell_term(int c, int ea, double fa, int eb, double fb, int eN, double fN,
+// c * L for one cell; c == 0 contributes exactly 0 (0 * log 0 = 0).
+__device__ __forceinline__ double cell_term(double c, double eab, double fa, double fb, double fN,
                                             const double2* __restrict__ tab) {
-    const double dc = (double)(c > 0 ? c : 1);
-    int ec;
-    const double fc = log2_frac(dc, tab, ec);
-    const double L = (double)(ec + eN - ea - eb) + (((fc + fN) - fa) - fb);
-    return c > 0 ? dc * L : 0.0;
+    const double cs = c > 0.0 ? c : 1.0;
+    const int hi = __double2hiint(cs);
+    const int lo = __double2loint(cs);
+    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);  // mantissa in [1, 2)
+    const double2 t = tab[(hi >> 13) & 127];
+    const double u = fma(m, t.x, -1.0);
+    double p = fma(u, kLog2C8, kLog2C7);
+    p = fma(u, p, kLog2C6);
+    p = fma(u, p, kLog2C5);
+    p = fma(u, p, kLog2C4);
+    p = fma(u, p, kLog2C3);
+    p = fma(u, p, kLog2C2);
+    p = fma(u, p, kLog2C1);
+    const double fc = fma(u, p, t.y);                                         // log2(mantissa)
+    const double ec = u32_to_double((uint32_t)hi >> 20) - 1023.0;             // exponent, exact
+    const double L = (ec + eab) + (((fc + fN) - fa) - fb);
+    return __dmul_rn(c, L);  // explicit rounding: no FMA contraction with the running sum,
+}                            // so every call site (both diagonal orientations) agrees bitwise
+
+// s / N, correctly rounded: q = s * RN(1/N) refined by one exact-remainder step.
+__device__ __forceinline__ double div_n(double s, double dN, double rN) {
+    const double q = s * rN;
+    const double r = fma(-q, dN, s);
+    return fma(r, rN, q);
 }
 
-__device__ __forceinline__ double mi_exact(int g, const Marg& A, const Marg& B, int N, double dN, int eN,
-                                           double fN, const double2* __restrict__ tab) {
-    double s = cell_term(g, A.e1, A.f1, B.e1, B.f1, eN, fN, tab);                   // (1,1)
-    s += cell_term(A.v - g, A.e1, A.f1, B.e0, B.f0, eN, fN, tab);                   // (1,0)
-    s += cell_term(B.v - g, A.e0, A.f0, B.e1, B.f1, eN, fN, tab);                   // (0,1)
-    s += cell_term(N - A.v - B.v + g, A.e0, A.f0, B.e0, B.f0, eN, fN, tab);         // (0,0)
-    return s / dN;
+__device__ __forceinline__ double mi_exact(double g, const RowMarg& A, const ColStat& B, double fN,
+                                           double dN, double rN, const double2* __restrict__ tab) {
+    const double c10 = A.v - g;
+    const double c01 = B.v - g;
+    const double c00 = (A.nv - B.v) + g;
+    double s = cell_term(g, A.er1 - B.e1, A.f1, B.f1, fN, tab);               // (1,1)
+    s = __dadd_rn(s, cell_term(c10, A.er1 - B.e0, A.f1, B.f0, fN, tab));      // (1,0)
+    s = __dadd_rn(s, cell_term(c01, A.er0 - B.e1, A.f0, B.f1, fN, tab));      // (0,1)
+    s = __dadd_rn(s, cell_term(c00, A.er0 - B.e0, A.f0, B.f0, fN, tab));      // (0,0)
+    return div_n(s, dN, rN);
 }
 
 // Epsilon mode (engine.py:112-113): p * log2((p + eps) / (e + eps)) with
 // p = count / n and e = (a / n)(b / n), evaluated with the reference's operations.
-__device__ __forceinline__ double mi_epsilon(int g, int vi, int vj, int N, double dN, double eps) {
-    const double a1 = (double)vi, a0 = (double)(N - vi), b1 = (double)vj, b0 = (double)(N - vj);
+__device__ __forceinline__ double mi_epsilon(double g, double vi, double vj, double dN, double eps) {
+    const double a1 = vi, a0 = dN - vi, b1 = vj, b0 = dN - vj;
     const double pa1 = a1 / dN, pa0 = a0 / dN, pb1 = b1 / dN, pb0 = b0 / dN;
-    double p, s;
-    p = (double)g / dN;                s = p * log2((p + eps) / (pa1 * pb1 + eps));
-    p = (double)(vi - g) / dN;         s += p * log2((p + eps) / (pa1 * pb0 + eps));
-    p = (double)(vj - g) / dN;         s += p * log2((p + eps) / (pa0 * pb1 + eps));
-    p = (double)(N - vi - vj + g) / dN; s += p * log2((p + eps) / (pa0 * pb0 + eps));
+    // explicit roundings (no FMA contraction), like the reference's NumPy ops
+    auto term = [&](double c, double pa, double pb) {
+        const double p = c / dN;
+        const double e = __dadd_rn(__dmul_rn(pa, pb), eps);
+        return __dmul_rn(p, log2(__dadd_rn(p, eps) / e));
+    };
+    double s = term(g, pa1, pb1);
+    s = __dadd_rn(s, term(vi - g, pa1, pb0));
+    s = __dadd_rn(s, term(vj - g, pa0, pb1));
+    s = __dadd_rn(s, term((dN - vi - vj) + g, pa0, pb0));
     return s;
 }
 
@@ -125,26 +155,67 @@ template <> struct OutT<MI_OUT_COUNTS> { using T = int32_t; };
 template <> struct OutT<MI_OUT_F64> { using T = double; };
 template <> struct OutT<MI_OUT_F32> { using T = float; };
 
+__device__ __forceinline__ void store_pair(double* p, double a, double b) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ void store_pair(float* p, float a, float b) {
+    *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
+__device__ __forceinline__ void store_pair(int32_t* p, int32_t a, int32_t b) {
+    *reinterpret_cast<int2*>(p) = make_int2(a, b);
+}
 
-// 32 consecutive outputs of one thread as 16-byte vector stores.
-__device__ __forceinline__ void store_row32(double* dst, const double (&v)[32]) {
+// 16 columns of one output row (this thread's TMEM lane): MI (or counts), the
+// direct store of row i and the coalesced mirror store of column i.
+template <int OUT, int MODE, bool DIAG, typename T>
+__device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A,
+                                           const ColStat* __restrict__ cols, const ColStat& Arow,
+                                           const GramMiParams& p, double eN, double fN, double dN, double rN,
+                                           const double2* __restrict__ tab, T* __restrict__ out, int64_t ld,
+                                           bool row_ok, bool vec_ok) {
+    const int m = p.m;
 #pragma unroll
-    for (int k = 0; k < 32; k += 2) *reinterpret_cast<double2*>(dst + k) = make_double2(v[k], v[k + 1]);
-}
-__device__ __forceinline__ void store_row32(float* dst, const float (&v)[32]) {
+    for (int k = 0; k < 16; k += 2) {
+        T v2[2];
 #pragma unroll
-    for (int k = 0; k < 32; k += 4)
-        *reinterpret_cast<float4*>(dst + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
-}
-__device__ __forceinline__ void store_row32(int32_t* dst, const int32_t (&v)[32]) {
-#pragma unroll
-    for (int k = 0; k < 32; k += 4)
-        *reinterpret_cast<int4*>(dst + k) = make_int4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+        for (int h = 0; h < 2; ++h) {
+            const int j = j0 + k + h;
+            if constexpr (OUT == MI_OUT_COUNTS) {
+                v2[h] = (T)r[k + h];
+            } else {
+                const double g = u32_to_double(r[k + h]);
+                const ColStat& B = cols[k + h];
+                double x;
+                if constexpr (MODE == MI_MODE_EXACT) {
+                    if (DIAG && j < i) {
+                        // (min, max) orientation: the two halves of a diagonal
+                        // tile are then bit-identical mirrors
+                        x = mi_exact(g, row_marg(B, eN), Arow, fN, dN, rN, tab);
+                    } else {
+                        x = mi_exact(g, A, B, fN, dN, rN, tab);
+                    }
+                } else {
+                    x = (DIAG && j < i) ? mi_epsilon(g, B.v, A.v, dN, p.eps) : mi_epsilon(g, A.v, B.v, dN, p.eps);
+                }
+                if (DIAG && !p.include_diagonal && i == j) x = 0.0;
+                v2[h] = (T)x;
+            }
+            if (!DIAG && row_ok && j < m) out[(int64_t)j * ld + i] = v2[h];  // mirror, coalesced
+        }
+        if (row_ok) {
+            T* dst = out + (int64_t)i * ld + j0 + k;
+            if (vec_ok && j0 + k + 1 < m) {
+                store_pair(dst, v2[0], v2[1]);
+            } else {
+                if (j0 + k < m) dst[0] = v2[0];
+                if (j0 + k + 1 < m) dst[1] = v2[1];
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------- the kernel
 
-template <int CG>
 struct TileWalk {
     // Linear walk over (my tile, k-block) pairs: step g -> tile index, k-block.
     int cluster, n_clusters, n_tiles, nkb;
@@ -156,56 +227,29 @@ struct TileWalk {
     }
 };
 
-// One 32-column chunk of the epilogue for one thread (= one output row).
-template <int OUT, int MODE, bool DIAG, typename T>
-__device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int i, int j0, const Marg& Ar,
-                                               const GramMiParams& p, int eN, double fN, double dN,
-                                               const double2* __restrict__ tab, T (&val)[32]) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        const int j = j0 + k;
-        const int g = (int)r[k];
-        if constexpr (OUT == MI_OUT_COUNTS) {
-            val[k] = g;
-        } else {
-            const Marg Bc = load_marg(p.colstat, j);
-            // Each element is evaluated in (min, max) orientation so the two
-            // halves of a diagonal tile are bit-identical mirrors.
-            const bool sw = DIAG && (j < i);
-            double x;
-            if constexpr (MODE == MI_MODE_EXACT) {
-                x = sw ? mi_exact(g, Bc, Ar, p.n_rows, dN, eN, fN, tab)
-                       : mi_exact(g, Ar, Bc, p.n_rows, dN, eN, fN, tab);
-            } else {
-                x = mi_epsilon(g, sw ? Bc.v : Ar.v, sw ? Ar.v : Bc.v, p.n_rows, dN, p.eps);
-            }
-            if (DIAG && !p.include_diagonal && i == j) x = 0.0;
-            val[k] = (T)x;
-        }
-    }
-}
-
-template <int CG, int OUT, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int CG, int OUT, int MODE, int ST, int EW>
+__global__ void __launch_bounds__(Cfg<CG, EW>::THREADS, 1)
 gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p) {
-    using C = Cfg<CG>;
+    using C = Cfg<CG, EW>;
     using T = typename OutT<OUT>::T;
+    using L = SmemLayout<CG, ST>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     const uint32_t base = (raw_addr + 1023u) & ~1023u;  // SW128 needs 1024-B alignment
+    if (base - raw_addr + L::bytes > L::request) __trap();
     uint8_t* const smem = smem_raw + (base - raw_addr);
 
-    const uint32_t sA = base + SmemLayout::a_off;
-    const uint32_t sB = base + SmemLayout::b_off;
-    const uint32_t bar0 = base + SmemLayout::bar_off;
-    double2* const tab = reinterpret_cast<double2*>(smem + SmemLayout::tab_off);
+    const uint32_t sA = base + L::a_off;
+    const uint32_t sB = base + L::b_off;
+    const uint32_t bar0 = base + L::bar_off;
+    double2* const tab = reinterpret_cast<double2*>(smem + L::tab_off);
+    ColStat* const colbuf = reinterpret_cast<ColStat*>(smem + L::col_off);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
-    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * kStages + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * kStages + 2 + a); };
-    const uint32_t tmem_slot = bar0 + 8u * (2 * kStages + 4);
-    volatile uint32_t* tmem_slot_ptr =
-        reinterpret_cast<volatile uint32_t*>(smem + SmemLayout::bar_off + 8 * (2 * kStages + 4));
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * ST + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * ST + 2 + a); };
+    const uint32_t tmem_slot = bar0 + 8u * (2 * ST + 4);
+    volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(smem + L::bar_off + 8 * (2 * ST + 4));
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
@@ -216,26 +260,26 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     // ---- one-time setup
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_x);
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < ST; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), CG * kNumEpiWarps);
+            mbar_init(tempty_bar(a), CG * EW);
         }
         fence_mbarrier_init();
     }
-    if (threadIdx.x >= kEpiWarp0 * 32 && threadIdx.x < kEpiWarp0 * 32 + 128)
-        tab[threadIdx.x - kEpiWarp0 * 32] = kLog2TabInit[threadIdx.x - kEpiWarp0 * 32];
-    if (warp == 2) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+    const int etid = (int)threadIdx.x - kEpiWarp0 * 32;  // epilogue thread id (may be < 0)
+    if (etid >= 0 && etid < 128) tab[etid] = kLog2TabInit[etid];
+    if (warp == 1) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
 
     const int nkb = p.num_k_blocks;
-    const TileWalk<CG> walk{cluster, n_clusters, p.n_tiles, nkb};
+    const TileWalk walk{cluster, n_clusters, p.n_tiles, nkb};
 
     if (warp == 0) {
         // ================= TMA producer =================
@@ -247,8 +291,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             const uint32_t fb_rank = (CG == 2) ? 0u : rank;  // CG == 2: signal the leader's barrier
             int s = 0;
             uint32_t ph = 0;
-            // warm the L2 with the first kPrefetchDist k-blocks
-            for (long long g = 0; g < pf; ++g) {
+            for (long long g = 0; g < pf; ++g) {  // warm the L2 with the first pf k-blocks
                 int t, kb;
                 if (!walk.at(g, t, kb)) break;
                 const int2 tile = p.tiles[t];
@@ -271,12 +314,12 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
                 tma_load_3d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, 0, rowA, kb, policy);
                 tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
-                if (++s == kStages) { s = 0; ph ^= 1u; }
+                if (++s == ST) { s = 0; ph ^= 1u; }
             }
             // drain: the last commit of every stage must land before exit
-            for (int q = 0; q < kStages; ++q) {
+            for (int q = 0; q < ST; ++q) {
                 mbar_wait(empty_bar(s), ph ^ 1u);
-                if (++s == kStages) { s = 0; ph ^= 1u; }
+                if (++s == ST) { s = 0; ph ^= 1u; }
             }
         }
     } else if (warp == 1) {
@@ -299,26 +342,27 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 #pragma unroll
                     for (int k = 0; k < kBK / 32; ++k) {
                         // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
-                        umma_i8<CG>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc,
-                                    (kb | k) != 0 ? 1u : 0u);
+                        umma_i8<CG>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
                     umma_commit<CG>(empty_bar(s));  // frees the smem slot (both CTAs)
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
+                    if (++s == ST) { s = 0; ph ^= 1u; }
                 }
                 umma_commit<CG>(tfull_bar(acc));  // accumulator ready (both CTAs)
                 if (++acc == 2) { acc = 0; aph ^= 1u; }
             }
         }
-    } else if (warp >= kEpiWarp0) {
+    } else {
         // ================= epilogue =================
-        named_barrier_sync(1, kNumEpiWarps * 32);  // log2 table is in smem
-        const int q = warp & 3;                    // TMEM lane quadrant of this warp
-        const int h = (warp - kEpiWarp0) >> 2;     // which half of the accumulator columns
+        const int q = warp & 3;                          // TMEM lane quadrant of this warp
+        const int part = (warp - kEpiWarp0) >> 2;        // which column slice of the accumulator
         const int row_local = q * 32 + (int)lane;
         const int m = p.m;
         const double dN = (double)p.n_rows;
-        int eN;
-        const double fN = log2_frac(dN, tab, eN);  // same routine as the per-column logs
+        const double rN = 1.0 / dN;
+        named_barrier_sync(1, EW * 32);                  // log2 table is in smem
+        int eNi;
+        const double fN = log2_frac(dN, tab, eNi);       // same routine as the per-column logs
+        const double eN = (double)eNi;
         const int64_t ld = p.ld_out;
         T* __restrict__ out = reinterpret_cast<T*>(p.out);
         const uint32_t tempty_leader0 = (CG == 2) ? map_to_cta(tempty_bar(0), 0) : tempty_bar(0);
@@ -329,41 +373,31 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             const int2 tile = p.tiles[t];
             const bool diag = tile.x == tile.y;
             const int i = tile.x * C::TS + (int)rank * 128 + row_local;
-            Marg Ar{0.0, 0.0, 0, 0, 0};
-            if constexpr (OUT != MI_OUT_COUNTS) Ar = load_marg(p.colstat, i);  // colstat has m_pad rows
+            ColStat* const cols = colbuf + acc * C::TS;   // this tile's column marginals
+            if constexpr (OUT != MI_OUT_COUNTS) {
+                if (etid < C::TS) cols[etid] = p.colstat[tile.y * C::TS + etid];
+                named_barrier_sync(2, EW * 32);
+            }
+            ColStat Arow{};
+            if constexpr (OUT != MI_OUT_COUNTS) Arow = p.colstat[i];  // colstat has m_pad entries
+            const RowMarg A = row_marg(Arow, eN);
+            const bool row_ok = i < m;
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < C::CHUNKS; ++c) {
-                const int col0 = h * C::HALF_COLS + c * 32;
+            for (int c = 0; c < C::WARP_COLS; c += 16) {
+                const int col0 = part * C::WARP_COLS + c;
                 const int j0 = tile.y * C::TS + col0;
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
-                                       (uint32_t)(acc * C::ACC_COLS + col0),
-                                   r);
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + col0), r);
                 tmem_ld_wait(r);
-                T val[32];
+                const bool vec_ok = ((reinterpret_cast<uintptr_t>(out + (int64_t)i * ld + j0) & (2 * sizeof(T) - 1)) == 0);
                 if (diag)
-                    epilogue_chunk<OUT, MODE, true>(r, i, j0, Ar, p, eN, fN, dN, tab, val);
+                    epilogue16<OUT, MODE, true>(r, i, j0, A, cols + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
+                                                row_ok, vec_ok);
                 else
-                    epilogue_chunk<OUT, MODE, false>(r, i, j0, Ar, p, eN, fN, dN, tab, val);
-                if (i < m) {
-                    // direct tile: row i, columns j0 .. j0+31
-                    T* dst = out + (int64_t)i * ld + j0;
-                    if (j0 + 32 <= m && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                        store_row32(dst, val);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            if (j0 + k < m) dst[k] = val[k];
-                    }
-                    // mirror tile: row j, column i (coalesced across the warp)
-                    if (!diag) {
-#pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            if (j0 + k < m) out[(int64_t)(j0 + k) * ld + i] = val[k];
-                    }
-                }
+                    epilogue16<OUT, MODE, false>(r, i, j0, A, cols + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
+                                                 row_ok, vec_ok);
             }
             // hand the accumulator back to the MMA warp
             tc_fence_before();
@@ -378,25 +412,24 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
-    if (warp == 2) tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+    if (warp == 1) tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
 }
 
 // ---------------------------------------------------------------- launch
 
-template <int CG, int OUT, int MODE>
-static cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_sms,
-                               cudaStream_t stream) {
-    auto kern = gram_mi_kernel<CG, OUT, MODE>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kSmemBytes);
+template <int CG, int OUT, int MODE, int ST, int EW>
+static cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream) {
+    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW>;
+    constexpr uint32_t smem = SmemLayout<CG, ST>::request;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int max_clusters = num_sms / CG;
     int clusters = p.n_tiles < max_clusters ? p.n_tiles : max_clusters;
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.blockDim = dim3(Cfg<CG, EW>::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -408,25 +441,29 @@ static cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, i
     return cudaLaunchKernelEx(&cfg, kern, tmap, p);
 }
 
-cudaError_t launch_gram_mi(int cg, int out_kind, int mode, const CUtensorMap& tmap,
+cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,
                            const GramMiParams& p, int num_sms, cudaStream_t stream) {
-#define MI_DISPATCH(CGV, OV, MV) \
-    if (cg == CGV && out_kind == OV && mode == MV) return launch_impl<CGV, OV, MV>(tmap, p, num_sms, stream);
-    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EXACT)
-    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EPSILON)
-    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT)
-    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EPSILON)
-    MI_DISPATCH(2, MI_OUT_COUNTS, MI_MODE_EXACT)
-    MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EXACT)
-    MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EPSILON)
-    MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EXACT)
-    MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EPSILON)
-    MI_DISPATCH(1, MI_OUT_COUNTS, MI_MODE_EXACT)
+#define MI_DISPATCH(CGV, OV, MV, STV, EWV)                                                       \
+    if (cg == CGV && out_kind == OV && mode == MV && stages == STV && epi_warps == EWV) \
+        return launch_impl<CGV, OV, MV, STV, EWV>(tmap, p, num_sms, stream);
+    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EXACT, 6, 8)
+    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EPSILON, 6, 8)
+    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8)
+    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EPSILON, 6, 8)
+    MI_DISPATCH(2, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
+    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EXACT, 6, 16)
+    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT, 6, 16)
+    MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EXACT, 6, 8)
+    MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EPSILON, 6, 8)
+    MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EXACT, 6, 8)
+    MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EPSILON, 6, 8)
+    MI_DISPATCH(1, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
 #undef MI_DISPATCH
+    // knob combinations without a dedicated build fall back to the default build of the variant
+    if (stages != 6 || epi_warps != 8) return launch_gram_mi(cg, out_kind, mode, 6, 8, tmap, p, num_sms, stream);
     return cudaErrorInvalidValue;
 }
 
 int gram_mi_tile_size(int cg) { return 128 * cg; }
-uint32_t gram_mi_smem_bytes() { return kSmemBytes; }
 
 }  // namespace mib200

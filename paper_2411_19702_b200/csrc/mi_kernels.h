@@ -29,10 +29,9 @@ struct GramMiParams {
     int l2_hint;            // 0 normal, 1 evict_last, 2 evict_first for operand loads
 };
 
-cudaError_t launch_gram_mi(int cg, int out_kind, int mode, const CUtensorMap& tmap,
+cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,
                            const GramMiParams& p, int num_sms, cudaStream_t stream);
 int gram_mi_tile_size(int cg);
-uint32_t gram_mi_smem_bytes();
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
                                  int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,

@@ -60,13 +60,14 @@ unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t n_rows, int64_t
             if (colsum) colsum[c] = (int32_t)cnt;
             // marginal logs for the fused epilogue: log2(v) and log2(N - v)
             ColStat st;
-            st.v = (int)cnt;
-            st.pad = 0;
-            const int v0 = (int)(n_rows - (int64_t)cnt);
-            st.f1 = cnt > 0 ? log2_frac((double)cnt, kLog2TabInit, st.e1) : 0.0;
-            if (cnt == 0) st.e1 = 0;
-            st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, st.e0) : 0.0;
-            if (v0 <= 0) st.e0 = 0;
+            const int64_t v0 = n_rows - (int64_t)cnt;
+            int e1 = 0, e0 = 0;
+            st.v = (double)cnt;
+            st.nv = (double)v0;
+            st.f1 = cnt > 0 ? log2_frac((double)cnt, kLog2TabInit, e1) : 0.0;
+            st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, e0) : 0.0;
+            st.e1 = cnt > 0 ? (double)e1 : 0.0;
+            st.e0 = v0 > 0 ? (double)e0 : 0.0;
             colstat[c] = st;
         }
     }

@@ -29,3 +29,10 @@ if len(bad):
 mi = e.all_pairs_device(e.upload(w), n, m).cpu().numpy()
 ref = O.c_mi_all_pairs(w, n)
 print("MI max err", np.abs(mi - ref).max(), "sym", np.array_equal(mi, mi.T))
+bad = np.argwhere(mi != mi.T)
+print("asymmetric elements:", len(bad))
+if len(bad):
+    for i, j in bad[:12]:
+        print(i, j, repr(mi[i, j]), repr(mi[j, i]), repr(ref[i, j]), "tile", i // 256, j // 256)
+    ii, jj = bad[:, 0], bad[:, 1]
+    print("diag-tile fraction", np.mean(ii // 256 == jj // 256), "i<j fraction", np.mean(ii < jj))

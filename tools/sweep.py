@@ -11,11 +11,14 @@ from paper_2411_19702_b200 import _native as nat
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="3")
-ap.add_argument("--prefetch", default="12")
+ap.add_argument("--prefetch", default="0")
 ap.add_argument("--l2hint", default="1")
 ap.add_argument("--band", default="8")
 ap.add_argument("--cg", default="2")
 ap.add_argument("--reps", type=int, default=0)
+ap.add_argument("--stages", default="6")
+ap.add_argument("--epi", default="8")
+ap.add_argument("--dtype", default="auto")
 a = ap.parse_args()
 ints = lambda s: [int(x) for x in s.split(",")]
 eng = MIEngine.get(0)
@@ -26,12 +29,14 @@ for cfg in ints(a.configs):
     n, m = rec["n"], rec["m"]
     w = datagen.generate_words_device(rec, dev)
     prep = eng.prepare(w, n, m)
-    dt = torch.float64 if datagen.CONFIGS[cfg]["out"] == "float64" else torch.float32
+    dt = {"auto": torch.float64 if datagen.CONFIGS[cfg]["out"] == "float64" else torch.float32,
+          "f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[a.dtype]
     out = torch.empty((m, m), dtype=dt, device=dev)
     reps = a.reps or {1: 50, 2: 50, 3: 10, 4: 3, 5: 2}[cfg]
     W = n * m * (m + 1) / 2
-    for cg, pf, hint, band in itertools.product(ints(a.cg), ints(a.prefetch), ints(a.l2hint), ints(a.band)):
-        nat.set_tuning(cta_group=cg, prefetch=pf, l2_hint=hint, band=band)
+    for cg, pf, hint, band, st, ew in itertools.product(ints(a.cg), ints(a.prefetch), ints(a.l2hint),
+                                                        ints(a.band), ints(a.stages), ints(a.epi)):
+        nat.set_tuning(cta_group=cg, prefetch=pf, l2_hint=hint, band=band, stages=st, epi_warps=ew)
         eng._tiles.clear()
         tiles = eng.tiles(m)
         eng.compute(prep, None, dt, tiles=tiles, out=out)
@@ -43,7 +48,7 @@ for cfg in ints(a.configs):
             e0.record(); eng.compute(prep, None, dt, tiles=tiles, out=out); e1.record()
             e1.synchronize(); ms.append(e0.elapsed_time(e1))
         best, avg = min(ms), sum(ms) / len(ms)
-        print(json.dumps({"cfg": cfg, "cg": cg, "prefetch": pf, "l2hint": hint, "band": band,
+        print(json.dumps({"cfg": cfg, "cg": cg, "prefetch": pf, "l2hint": hint, "band": band, "stages": st, "epi_warps": ew, "dtype": str(dt).split(".")[-1],
                           "ms_avg": round(avg, 4), "ms_min": round(best, 4),
                           "tops_avg": round(2 * W / avg / 1e9, 1)}), flush=True)
     del prep, out, w
