@@ -60,9 +60,10 @@ int mi_device_info(int device, int* num_sms, int* cc_major, int* cc_minor);
 int64_t mi_kmajor_ld(int64_t n_rows);
 /* padded column count m_pad (operand rows, multiple of the tile size) */
 int64_t mi_kmajor_rows(int64_t n_cols);
-/* bytes of the per-column statistics workspace (marginal counts and their
- * log2 splits) that kernel 1 writes and the fused kernel reads */
-int64_t mi_colstat_bytes(int64_t n_cols);
+/* bytes of the per-column statistics workspace that kernel 1 writes and the
+ * fused kernel reads: marginal counts, their log2 splits and fixed-point
+ * c*log2(c) marginal terms */
+int64_t mi_colstat_bytes(int64_t n_rows, int64_t n_cols);
 /* output tile edge (256: a 2-SM tcgen05 tile) */
 int mi_tile_size(void);
 /* number of upper-triangle tiles (I <= J) for m columns */
@@ -109,7 +110,9 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
  * 1 = 128x128 on one SM), "prefetch" (L2 prefetch distance in k-blocks),
  * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per
  * band of the tile order), "stages" (smem ring depth), "epi_warps" (8 or 16
- * epilogue warps).  Also settable as MI_B200_<KEY> env vars. */
+ * epilogue warps), "fixed" (exact-mode epilogue: 1 adaptive per tile, default;
+ * 0 FP64 only; 2 fixed-point table only), "table_thr" (adaptive threshold on
+ * the tile's column-sum spread).  Also settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key */
 /* release the cached device workspaces of mi_*_host */

@@ -51,7 +51,7 @@ SIGNATURES = {
     "mi_device_info": (_int, [_int, _vp, _vp, _vp]),
     "mi_kmajor_ld": (_i64, [_i64]),
     "mi_kmajor_rows": (_i64, [_i64]),
-    "mi_colstat_bytes": (_i64, [_i64]),
+    "mi_colstat_bytes": (_i64, [_i64, _i64]),
     "mi_tile_size": (_int, []),
     "mi_num_tiles": (_i64, [_i64]),
     "mi_tile_list": (_i64, [_i64, _int, _int, _int, _vp, _i64]),

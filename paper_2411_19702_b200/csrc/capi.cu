@@ -49,18 +49,21 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
                        env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8),
-                       env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8)};
+                       env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
+                       env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
 int prefetch_dist() { return tuning().prefetch; }
 int l2_hint() { return tuning().l2_hint; }
 int tile_band() { return tuning().band > 0 ? tuning().band : 8; }
+
+long long* g_trace = nullptr;  // experiments only (mi_debug_set_trace)
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -133,6 +136,29 @@ int make_tmap(CUtensorMap* tm, const int8_t* x, int64_t ld, int64_t m_pad) {
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(MI_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
     return MI_OK;
+}
+
+// The fixed-point c log2 c table follows the per-column stats in the colstat
+// workspace (see mi_colstat_bytes); nullptr when N is beyond the table path.
+long long* xlogx_ptr(void* colstat, int64_t n_rows, int64_t n_cols) {
+    if (n_rows < 1 || n_rows >= kXlogxMaxN) return nullptr;
+    return reinterpret_cast<long long*>(reinterpret_cast<char*>(colstat) +
+                                        mi_kmajor_rows(n_cols) * (int64_t)sizeof(ColStat));
+}
+
+// Per-128-column (min, max) column sums, after the table.
+int2* blkrange_ptr(void* colstat, int64_t n_rows, int64_t n_cols) {
+    long long* t = xlogx_ptr(colstat, n_rows, n_cols);
+    return t ? reinterpret_cast<int2*>(t + n_rows + 1) : nullptr;
+}
+
+// rcp = round(2^(62 + nb) / N) and off0 = -(nb - 2) - s for fixed_to_fp
+void fixed_point_consts(int64_t N, unsigned long long* rcp, int* off0) {
+    int nb = 0;
+    while (nb < 63 && (1ll << nb) <= N) ++nb;
+    const unsigned __int128 num = (unsigned __int128)1 << (62 + nb);
+    *rcp = (unsigned long long)((num + (unsigned __int128)(N / 2)) / (unsigned __int128)N);
+    *off0 = -(nb - 2) - xlogx_scale(N);
 }
 
 int check_shape(int64_t n_rows, int64_t n_cols) {
@@ -227,10 +253,11 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
     if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
     if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
-    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_cols)))) return rc;
+    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
     MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
     MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
-                                 (int32_t*)ws.colsum, (ColStat*)ws.colstat, info.num_sms, ws.stream));
+                                 (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
+                                 blkrange_ptr(ws.colstat, n_rows, n_cols), info.num_sms, ws.stream));
     *ld_out = ld;
     *m_pad_out = m_pad;
     return MI_OK;
@@ -284,7 +311,11 @@ int64_t mi_kmajor_ld(int64_t n_rows) { return round_up(n_rows < 1 ? 1 : n_rows, 
 
 int64_t mi_kmajor_rows(int64_t n_cols) { return round_up(n_cols < 1 ? 1 : n_cols, 256); }
 
-int64_t mi_colstat_bytes(int64_t n_cols) { return mi_kmajor_rows(n_cols) * (int64_t)sizeof(ColStat); }
+int64_t mi_colstat_bytes(int64_t n_rows, int64_t n_cols) {
+    const int64_t stats = mi_kmajor_rows(n_cols) * (int64_t)sizeof(ColStat);
+    const int64_t table = (n_rows >= 1 && n_rows < kXlogxMaxN) ? (n_rows + 1) * 8 + mi_kmajor_rows(n_cols) / 128 * 8 : 0;
+    return stats + table;
+}
 
 int mi_tile_size(void) { return gram_mi_tile_size(cta_group()); }
 
@@ -325,7 +356,8 @@ int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, in
     const int64_t nw = (n_rows + 63) / 64;
     if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
     MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
-                                 (ColStat*)d_colstat, info.num_sms, (cudaStream_t)stream));
+                                 (ColStat*)d_colstat, xlogx_ptr(d_colstat, n_rows, n_cols),
+                                 blkrange_ptr(d_colstat, n_rows, n_cols), info.num_sms, (cudaStream_t)stream));
     return MI_OK;
 }
 
@@ -362,7 +394,16 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
     p.include_diagonal = include_diagonal ? 1 : 0;
     p.prefetch_dist = prefetch_dist();
     p.l2_hint = l2_hint();
-    const int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
+    p.debug = tuning().debug;
+    p.trace = g_trace;
+    fixed_point_consts(n_rows, &p.rcp, &p.off0);
+    p.fix_s = xlogx_scale(n_rows);
+    p.xlogx = xlogx_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+    p.blkrange = blkrange_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+    // exact-mode epilogue: 0 = FP64 only, 1 = adaptive per tile (default), 2 = table only
+    p.table_thr = tuning().fixed == 0 ? -1 : tuning().fixed == 2 ? 0x7FFFFFFF : tuning().table_thr;
+    int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
+    // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
     MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tuning().stages, tuning().epi_warps, tm, p, info.num_sms, (cudaStream_t)stream));
     return MI_OK;
 }
@@ -457,6 +498,11 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "stages")) {
         if (value != 6) return fail(MI_ERR_DOMAIN, "stages must be 6");
         t.stages = value;
+    } else if (!strcmp(key, "table_thr")) {
+        t.table_thr = value;
+    } else if (!strcmp(key, "fixed")) {
+        if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "fixed must be 0, 1 or 2");
+        t.fixed = value;
     } else if (!strcmp(key, "epi_warps")) {
         if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");
         t.epi_warps = value;
@@ -475,8 +521,14 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "band")) return t.band;
     if (!strcmp(key, "stages")) return t.stages;
     if (!strcmp(key, "epi_warps")) return t.epi_warps;
+    if (!strcmp(key, "fixed")) return t.fixed;
+    if (!strcmp(key, "table_thr")) return t.table_thr;
     return -1;
 }
+
+// Not part of the public header: route per-tile timestamps of cluster 0 into a
+// device buffer of 64 x 4 int64 (tools/trace_tiles.py), or nullptr to stop.
+void mi_debug_set_trace(void* d_buf) { g_trace = reinterpret_cast<long long*>(d_buf); }
 
 void mi_release_workspace(void) {
     std::lock_guard<std::mutex> lk(g_ws_mu);

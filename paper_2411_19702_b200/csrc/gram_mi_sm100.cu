@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "milog.cuh"
 #include "mi_kernels.h"
@@ -53,13 +54,24 @@ struct Cfg {
     static_assert(EW % 4 == 0 && WARP_COLS % 16 == 0, "bad epilogue split");
 };
 
+// Per-tile column marginals staged in shared memory by the epilogue: the
+// FP64-path logs and the fixed-point (table path) term of each column.
+struct ColS {
+    double v, e1, e0, f1, f0;  // v, and log2 v = e1 + f1, log2 (N - v) = e0 + f0
+    long long q;               // T(v) + T(N - v)
+    int vi, pad;
+};
+constexpr uint32_t kTabBytes = 128u * 16u;  // log2_frac double2 table
+
 template <int CG, int ST>
 struct SmemLayout {
+    static constexpr uint32_t CSZ = (uint32_t)sizeof(ColS);
+    static constexpr uint32_t TABB = kTabBytes;
     static constexpr uint32_t a_off = 0;
     static constexpr uint32_t b_off = ST * kStageHalfBytes;
-    static constexpr uint32_t tab_off = 2 * ST * kStageHalfBytes;  // log2 table, 2 KB
-    static constexpr uint32_t col_off = tab_off + 128 * 16;        // column stats [2][TS]
-    static constexpr uint32_t bar_off = col_off + 2 * 128 * CG * (uint32_t)sizeof(ColStat);
+    static constexpr uint32_t tab_off = 2 * ST * kStageHalfBytes;  // log tables
+    static constexpr uint32_t col_off = tab_off + TABB;            // column stats [2][TS]
+    static constexpr uint32_t bar_off = col_off + 2 * 128 * CG * CSZ;
     // full[ST], empty[ST], tfull[2], tempty[2], tmem slot
     static constexpr uint32_t bytes = bar_off + (2 * ST + 4) * 8 + 16;
     // + alignment slack when it fits (the dynamic window is normally 1 KB aligned)
@@ -86,9 +98,10 @@ struct RowMarg {        // the tile row's (A side) marginals
     double f1, f0;
 };
 
-__device__ __forceinline__ RowMarg row_marg(const ColStat& s, double eN) {
-    return RowMarg{s.v, s.nv, eN - s.e1, eN - s.e0, s.f1, s.f0};
+__device__ __forceinline__ RowMarg row_marg(const ColS& s, double eN, double dN) {
+    return RowMarg{s.v, dN - s.v, eN - s.e1, eN - s.e0, s.f1, s.f0};
 }
+__device__ __forceinline__ ColS col_s(const ColStat& s) { return ColS{s.v, s.e1, s.e0, s.f1, s.f0, s.q, s.vi, 0}; }
 
 // c * L for one cell; c == 0 contributes exactly 0 (0 * log 0 = 0).
 __device__ __forceinline__ double cell_term(double c, double eab, double fa, double fb, double fN,
@@ -119,7 +132,7 @@ __device__ __forceinline__ double div_n(double s, double dN, double rN) {
     return fma(r, rN, q);
 }
 
-__device__ __forceinline__ double mi_exact(double g, const RowMarg& A, const ColStat& B, double fN,
+__device__ __forceinline__ double mi_exact(double g, const RowMarg& A, const ColS& B, double fN,
                                            double dN, double rN, const double2* __restrict__ tab) {
     const double c10 = A.v - g;
     const double c01 = B.v - g;
@@ -165,51 +178,86 @@ __device__ __forceinline__ void store_pair(int32_t* p, int32_t a, int32_t b) {
     *reinterpret_cast<int2*>(p) = make_int2(a, b);
 }
 
+// The tile row's fixed-point marginals (table path).
+struct RowQ {
+    int v, nmv;      // v_i, N - v_i
+    long long kq;    // T(N) - (T(v_i) + T(N - v_i))
+};
+
 // 16 columns of one output row (this thread's TMEM lane): MI (or counts), the
-// direct store of row i and the coalesced mirror store of column i.
-template <int OUT, int MODE, bool DIAG, typename T>
-__device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A,
-                                           const ColStat* __restrict__ cols, const ColStat& Arow,
+// coalesced mirror store of column i and the direct store of row i.
+// TABLE: exact mode through the fixed-point c log2 c table (integer sums, no
+// FP64 -- B200 runs FP64 on the tensor datapath, ~23x slower under tcgen05.mma);
+// otherwise the FP64 epilogue (epsilon mode, and exact-mode tiles whose column
+// sums are too spread out for the table gathers to stay in L1).
+template <int OUT, int MODE, bool DIAG, bool TABLE, typename T>
+__device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A, const RowQ& AQ,
+                                           const ColS* __restrict__ cols, const ColS& Arow,
                                            const GramMiParams& p, double eN, double fN, double dN, double rN,
                                            const double2* __restrict__ tab, T* __restrict__ out, int64_t ld,
                                            bool row_ok, bool vec_ok) {
     const int m = p.m;
+    // 1) all 16 values into registers first: independent chains (and table
+    //    gathers) the scheduler can overlap, no stores in between
+    T v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int j = j0 + k;
+        if constexpr (OUT == MI_OUT_COUNTS) {
+            v[k] = (T)r[k];
+        } else if constexpr (TABLE) {
+            // integer sum of fixed-point terms: exact and order-independent, so
+            // both halves of a diagonal tile agree bit for bit
+            const int g = (int)r[k];
+            const int bv = cols[k].vi;
+            const long long* __restrict__ X = p.xlogx;
+            const long long S = (__ldg(X + g) + __ldg(X + (AQ.v - g))) +
+                                (__ldg(X + (bv - g)) + __ldg(X + (AQ.nmv - bv + g))) + (AQ.kq - cols[k].q);
+            T x = fixed_to_fp<T>(S, p.rcp, p.off0);
+            if (DIAG && !p.include_diagonal && i == j) x = (T)0;
+            v[k] = x;
+        } else {
+            const double g = u32_to_double(r[k]);
+            const ColS& B = cols[k];
+            double x;
+            if constexpr (MODE == MI_MODE_EXACT) {
+                if (DIAG && j < i) {
+                    // (min, max) orientation: the two halves of a diagonal
+                    // tile are then bit-identical mirrors
+                    x = mi_exact(g, row_marg(B, eN, dN), Arow, fN, dN, rN, tab);
+                } else {
+                    x = mi_exact(g, A, B, fN, dN, rN, tab);
+                }
+            } else {
+                x = (DIAG && j < i) ? mi_epsilon(g, B.v, A.v, dN, p.eps) : mi_epsilon(g, A.v, B.v, dN, p.eps);
+            }
+            if (DIAG && !p.include_diagonal && i == j) x = 0.0;
+            v[k] = (T)x;
+        }
+    }
+    if (p.debug) {  // keep the math alive without storing the tile
+        T acc = v[0];
+#pragma unroll
+        for (int k = 1; k < 16; ++k) acc = acc + v[k];
+        if (acc == (T)-12345) out[0] = acc;
+        return;
+    }
+    if (!row_ok) return;
+    // 2) mirror tile: row j, column i (coalesced across the warp)
+    if (!DIAG) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (j0 + k < m) out[(int64_t)(j0 + k) * ld + i] = v[k];
+    }
+    // 3) direct tile: row i, columns j0 .. j0+15
+    T* dst = out + (int64_t)i * ld + j0;
 #pragma unroll
     for (int k = 0; k < 16; k += 2) {
-        T v2[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int j = j0 + k + h;
-            if constexpr (OUT == MI_OUT_COUNTS) {
-                v2[h] = (T)r[k + h];
-            } else {
-                const double g = u32_to_double(r[k + h]);
-                const ColStat& B = cols[k + h];
-                double x;
-                if constexpr (MODE == MI_MODE_EXACT) {
-                    if (DIAG && j < i) {
-                        // (min, max) orientation: the two halves of a diagonal
-                        // tile are then bit-identical mirrors
-                        x = mi_exact(g, row_marg(B, eN), Arow, fN, dN, rN, tab);
-                    } else {
-                        x = mi_exact(g, A, B, fN, dN, rN, tab);
-                    }
-                } else {
-                    x = (DIAG && j < i) ? mi_epsilon(g, B.v, A.v, dN, p.eps) : mi_epsilon(g, A.v, B.v, dN, p.eps);
-                }
-                if (DIAG && !p.include_diagonal && i == j) x = 0.0;
-                v2[h] = (T)x;
-            }
-            if (!DIAG && row_ok && j < m) out[(int64_t)j * ld + i] = v2[h];  // mirror, coalesced
-        }
-        if (row_ok) {
-            T* dst = out + (int64_t)i * ld + j0 + k;
-            if (vec_ok && j0 + k + 1 < m) {
-                store_pair(dst, v2[0], v2[1]);
-            } else {
-                if (j0 + k < m) dst[0] = v2[0];
-                if (j0 + k + 1 < m) dst[1] = v2[1];
-            }
+        if (vec_ok && j0 + k + 1 < m) {
+            store_pair(dst + k, v[k], v[k + 1]);
+        } else {
+            if (j0 + k < m) dst[k] = v[k];
+            if (j0 + k + 1 < m) dst[k + 1] = v[k + 1];
         }
     }
 }
@@ -243,7 +291,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     const uint32_t sB = base + L::b_off;
     const uint32_t bar0 = base + L::bar_off;
     double2* const tab = reinterpret_cast<double2*>(smem + L::tab_off);
-    ColStat* const colbuf = reinterpret_cast<ColStat*>(smem + L::col_off);
+    ColS* const colbuf = reinterpret_cast<ColS*>(smem + L::col_off);
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * ST + a); };
@@ -330,9 +378,11 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             uint32_t ph = 0;
             int acc = 0;
             uint32_t aph = 0;
-            for (int t = cluster; t < p.n_tiles; t += n_clusters) {
+            int it = 0;
+            for (int t = cluster; t < p.n_tiles; t += n_clusters, ++it) {
                 mbar_wait(tempty_bar(acc), aph ^ 1u);
                 tc_fence_after();
+                if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 0] = clock64();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(full_bar(s), ph);
@@ -348,6 +398,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     if (++s == ST) { s = 0; ph ^= 1u; }
                 }
                 umma_commit<CG>(tfull_bar(acc));  // accumulator ready (both CTAs)
+                if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 1] = clock64();
                 if (++acc == 2) { acc = 0; aph ^= 1u; }
             }
         }
@@ -363,27 +414,57 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         int eNi;
         const double fN = log2_frac(dN, tab, eNi);       // same routine as the per-column logs
         const double eN = (double)eNi;
+        const bool have_table = MODE == MI_MODE_EXACT && p.xlogx != nullptr;
+        const long long nln = have_table ? p.xlogx[p.n_rows] : 0ll;  // T(N) = N log2 N 2^s
         const int64_t ld = p.ld_out;
         T* __restrict__ out = reinterpret_cast<T*>(p.out);
         const uint32_t tempty_leader0 = (CG == 2) ? map_to_cta(tempty_bar(0), 0) : tempty_bar(0);
         const uint32_t tempty_leader1 = (CG == 2) ? map_to_cta(tempty_bar(1), 0) : tempty_bar(1);
         int acc = 0;
         uint32_t aph = 0;
-        for (int t = cluster; t < p.n_tiles; t += n_clusters) {
+        int it = 0;
+        const bool tracer = p.trace && cluster == 0 && rank == 0 && warp == kEpiWarp0 && lane == 0;
+        for (int t = cluster; t < p.n_tiles; t += n_clusters, ++it) {
             const int2 tile = p.tiles[t];
             const bool diag = tile.x == tile.y;
             const int i = tile.x * C::TS + (int)rank * 128 + row_local;
-            ColStat* const cols = colbuf + acc * C::TS;   // this tile's column marginals
+            ColS* const cols = colbuf + acc * C::TS;   // this tile's column marginals
+            ColS Arow{};
+            RowQ AQ{0, 0, 0};
+            bool use_table = false;
             if constexpr (OUT != MI_OUT_COUNTS) {
-                if (etid < C::TS) cols[etid] = p.colstat[tile.y * C::TS + etid];
+                if (etid < C::TS) cols[etid] = col_s(p.colstat[tile.y * C::TS + etid]);
                 named_barrier_sync(2, EW * 32);
+                Arow = col_s(p.colstat[i]);  // colstat has m_pad entries
+                AQ = RowQ{Arow.vi, p.n_rows - Arow.vi, nln - Arow.q};
+                // per-tile choice (identical in both CTAs of a pair): table path
+                // when the tile's column sums are clustered enough for the
+                // gathers to hit in L1, FP64 path otherwise
+                if (have_table) {
+                    const int bl = C::TS / 128;
+                    int lo = 0x7FFFFFFF, hi = -1, spread = 0;
+                    for (int q2 = 0; q2 < bl; ++q2) {
+                        const int2 a = p.blkrange[tile.x * bl + q2];
+                        lo = min(lo, a.x);
+                        hi = max(hi, a.y);
+                    }
+                    spread = hi >= lo ? hi - lo : 0;
+                    lo = 0x7FFFFFFF;
+                    hi = -1;
+                    for (int q2 = 0; q2 < bl; ++q2) {
+                        const int2 a = p.blkrange[tile.y * bl + q2];
+                        lo = min(lo, a.x);
+                        hi = max(hi, a.y);
+                    }
+                    spread += hi >= lo ? hi - lo : 0;
+                    use_table = spread <= p.table_thr;
+                }
             }
-            ColStat Arow{};
-            if constexpr (OUT != MI_OUT_COUNTS) Arow = p.colstat[i];  // colstat has m_pad entries
-            const RowMarg A = row_marg(Arow, eN);
+            const RowMarg A = row_marg(Arow, eN, dN);
             const bool row_ok = i < m;
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
+            if (tracer && it < 64) p.trace[it * 4 + 2] = clock64();
 #pragma unroll 1
             for (int c = 0; c < C::WARP_COLS; c += 16) {
                 const int col0 = part * C::WARP_COLS + c;
@@ -392,14 +473,25 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + col0), r);
                 tmem_ld_wait(r);
                 const bool vec_ok = ((reinterpret_cast<uintptr_t>(out + (int64_t)i * ld + j0) & (2 * sizeof(T) - 1)) == 0);
-                if (diag)
-                    epilogue16<OUT, MODE, true>(r, i, j0, A, cols + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
-                                                row_ok, vec_ok);
-                else
-                    epilogue16<OUT, MODE, false>(r, i, j0, A, cols + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
-                                                 row_ok, vec_ok);
+                if (use_table) {
+                    if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
+                        if (diag)
+                            epilogue16<OUT, MODE, true, true>(r, i, j0, A, AQ, cols + col0, Arow, p, eN, fN, dN, rN, tab,
+                                                              out, ld, row_ok, vec_ok);
+                        else
+                            epilogue16<OUT, MODE, false, true>(r, i, j0, A, AQ, cols + col0, Arow, p, eN, fN, dN, rN, tab,
+                                                               out, ld, row_ok, vec_ok);
+                    }
+                } else if (diag) {
+                    epilogue16<OUT, MODE, true, false>(r, i, j0, A, AQ, cols + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
+                                                       row_ok, vec_ok);
+                } else {
+                    epilogue16<OUT, MODE, false, false>(r, i, j0, A, AQ, cols + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
+                                                        row_ok, vec_ok);
+                }
             }
             // hand the accumulator back to the MMA warp
+            if (tracer && it < 64) p.trace[it * 4 + 3] = clock64();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
@@ -451,8 +543,6 @@ cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_w
     MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8)
     MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EPSILON, 6, 8)
     MI_DISPATCH(2, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
-    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EXACT, 6, 16)
-    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT, 6, 16)
     MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EXACT, 6, 8)
     MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EPSILON, 6, 8)
     MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EXACT, 6, 8)

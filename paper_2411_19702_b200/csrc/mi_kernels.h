@@ -10,6 +10,7 @@
 #define MI_MODE_EXACT 0
 #define MI_MODE_EPSILON 1
 
+
 namespace mib200 {
 
 struct ColStat;
@@ -27,7 +28,16 @@ struct GramMiParams {
     int include_diagonal;
     int prefetch_dist;      // k-blocks of L2 prefetch ahead of the TMA ring (0 = off)
     int l2_hint;            // 0 normal, 1 evict_last, 2 evict_first for operand loads
+    int debug;              // experiments only: 1 = compute but skip the output stores
+    long long* trace;       // experiments only: per-tile timestamps of cluster 0 (or nullptr)
+    unsigned long long rcp; // fixed point: round(2^(62 + nb) / N), nb = bit length of N
+    int off0;               // fixed point: -(nb - 2) - s
+    int fix_s;              // fixed point: scale s of the c log2 c terms
+    const long long* xlogx; // exact mode: fixed-point T(c) = c log2(c) 2^s, c = 0..N (or nullptr)
+    const int2* blkrange;   // exact mode: (min, max) column sum per 128-column block
+    int table_thr;          // table path when the tile's two column-sum ranges sum to <= this
 };
+constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
 
 cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,
                            const GramMiParams& p, int num_sms, cudaStream_t stream);
@@ -35,7 +45,8 @@ int gram_mi_tile_size(int cg);
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
                                  int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,
-                                 ColStat* colstat, int num_sms, cudaStream_t stream);
+                                 ColStat* colstat, long long* xlogx, int2* blkrange, int num_sms,
+                                 cudaStream_t stream);
 
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,
                                   const uint64_t* col_threshold, const uint8_t* col_kind,

@@ -25,10 +25,27 @@ namespace mib200 {
 // so the multiply places bit k at bit 8k with no carries).
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
+// T(c) = c log2(c) 2^s for c = 0..N with the epilogue's own fix_xlog2x, so the
+// table path and the per-column terms agree bit for bit.
+__global__ void __launch_bounds__(256) xlogx_table_kernel(long long* __restrict__ T, long long N, int s,
+                                                          int2* __restrict__ blkrange, int nblk) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
+        blkrange[b] = make_int2(0x7FFFFFFF, -1);  // (min, max) column sum, filled by the unpack
+    __shared__ float R[1 << kFixLogBits];
+    __shared__ float2 LG[1 << kFixLogBits];
+    for (int q = threadIdx.x; q < (1 << kFixLogBits); q += blockDim.x) {
+        R[q] = kFixR[q];
+        LG[q] = kFixLG[q];
+    }
+    __syncthreads();
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c <= N; c += (long long)gridDim.x * blockDim.x)
+        T[c] = fix_xlog2x((unsigned)c, s, R, LG);
+}
+
 __global__ void __launch_bounds__(256)
 unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t n_rows, int64_t m, int64_t nw,
                      int8_t* __restrict__ x, int64_t ld, int64_t m_pad, int32_t* __restrict__ colsum,
-                     ColStat* __restrict__ colstat) {
+                     ColStat* __restrict__ colstat, int fix_s, int2* __restrict__ blkrange) {
     const int lane = threadIdx.x & 31;
     const int quarter = lane & 3;
     const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -68,21 +85,35 @@ unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t n_rows, int64_t
             st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, e0) : 0.0;
             st.e1 = cnt > 0 ? (double)e1 : 0.0;
             st.e0 = v0 > 0 ? (double)e0 : 0.0;
+            st.vi = (int)cnt;
+            st.pad = 0;
+            st.q = fix_xlog2x(cnt, fix_s, kFixR, kFixLG) + fix_xlog2x((unsigned)v0, fix_s, kFixR, kFixLG);
+            if (blkrange && real) {
+                atomicMin(&blkrange[c / 128].x, (int)cnt);
+                atomicMax(&blkrange[c / 128].y, (int)cnt);
+            }
             colstat[c] = st;
         }
     }
 }
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
-                                 int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, int num_sms,
-                                 cudaStream_t stream) {
+                                 int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, long long* xlogx,
+                                 int2* blkrange, int num_sms, cudaStream_t stream) {
+    if (xlogx) {
+        int64_t tb = (n_rows + 1 + 255) / 256;
+        if (tb > (int64_t)num_sms * 16) tb = (int64_t)num_sms * 16;
+        xlogx_table_kernel<<<(unsigned)tb, 256, 0, stream>>>(xlogx, n_rows, xlogx_scale(n_rows), blkrange,
+                                                              blkrange ? (int)(m_pad / 128) : 0);
+    }
     const int threads = 256;
     int64_t blocks = (m_pad + 7) / 8;
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     unpack_colsum_kernel<<<(unsigned)blocks, threads, 0, stream>>>(words, n_rows, m, nw, x, ld, m_pad, colsum,
-                                                                   colstat);
+                                                                   colstat, xlogx_scale(n_rows),
+                                                                   xlogx ? blkrange : nullptr);
     return cudaGetLastError();
 }
 

@@ -154,7 +154,7 @@ class MIEngine:
         ld, m_pad = self.layout(n_rows, n_cols)
         x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
         colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
-        colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_cols)),), dtype=torch.uint8, device=self.device)
+        colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_rows, n_cols)),), dtype=torch.uint8, device=self.device)
         nat.check(nat.lib().mi_unpack_colsum(words_dev.data_ptr(), n_rows, n_cols, x.data_ptr(), ld,
                                              colstat.data_ptr(), colsum.data_ptr(), _stream_ptr(self.device)),
                   "mi_unpack_colsum")
