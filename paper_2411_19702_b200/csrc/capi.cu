@@ -10,7 +10,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/mimatrix_b200.h"
@@ -18,6 +20,11 @@
 #include "milog.cuh"
 
 using namespace mib200;
+
+// fused kernel launch shared by mi_gram_mi and the host entry points (defined below)
+int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
+                 double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const int32_t* d_tiles,
+                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream);
 
 namespace {
 
@@ -193,15 +200,20 @@ int check_padding(const uint64_t* h_words, int64_t n_rows, int64_t n_cols) {
 
 // Banded upper-triangle order: within a band of `band` tile rows, sweep J and
 // then the band's rows, so tiles that run concurrently share operand blocks.
-std::vector<int32_t> all_tiles(int64_t T, int band) {
+// `first` > 0 makes the first band that many rows (1 for the host path: tile
+// row 0 then completes in the first wave and the D2H of finished rows starts).
+std::vector<int32_t> all_tiles(int64_t T, int band, int first = 0) {
     std::vector<int32_t> v;
     v.reserve((size_t)(T * (T + 1)));
-    for (int64_t I0 = 0; I0 < T; I0 += band)
+    for (int64_t I0 = 0; I0 < T;) {
+        const int64_t b = (I0 == 0 && first > 0) ? first : band;
         for (int64_t J = I0; J < T; ++J)
-            for (int64_t I = I0; I < I0 + band && I <= J; ++I) {
+            for (int64_t I = I0; I < I0 + b && I <= J; ++I) {
                 v.push_back((int32_t)I);
                 v.push_back((int32_t)J);
             }
+        I0 += b;
+    }
     return v;
 }
 
@@ -215,6 +227,10 @@ struct Workspace {
     void* colstat = nullptr; size_t colstat_cap = 0;
     void* tiles = nullptr; size_t tiles_cap = 0;
     void* out = nullptr; size_t out_cap = 0;
+    cudaStream_t copy_stream = nullptr;   // D2H of finished row bands
+    unsigned int* row_done_h = nullptr;   // pinned, mapped: per tile row completion counts
+    unsigned int* row_done_d = nullptr;   // device alias of row_done_h
+    size_t row_done_cap = 0;
 };
 std::mutex g_ws_mu;
 Workspace g_ws[64];
@@ -239,6 +255,9 @@ void release(Workspace& w) {
         if (*p) cudaFree(*p), *p = nullptr;
     w.words_cap = w.x_cap = w.colsum_cap = w.colstat_cap = w.tiles_cap = w.out_cap = 0;
     if (w.stream) cudaStreamDestroy(w.stream), w.stream = nullptr;
+    if (w.copy_stream) cudaStreamDestroy(w.copy_stream), w.copy_stream = nullptr;
+    if (w.row_done_h) cudaFreeHost(w.row_done_h), w.row_done_h = nullptr, w.row_done_d = nullptr;
+    w.row_done_cap = 0;
     w.device = -1;
     cudaSetDevice(prev);
 }
@@ -271,22 +290,24 @@ int workspace_for(int device, Workspace** out, DevInfo* info) {
     if (ws.device < 0) {
         ws.device = device;
         MI_CUDA(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+        MI_CUDA(cudaStreamCreateWithFlags(&ws.copy_stream, cudaStreamNonBlocking));
     }
     *out = &ws;
     return MI_OK;
 }
 
 int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t m_pad, int mode, double eps,
-              int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const DevInfo& info) {
+              int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const DevInfo& info,
+              unsigned int* row_done = nullptr) {
     (void)m_pad;
     const int64_t n_tiles = mi_num_tiles(n_cols);
-    std::vector<int32_t> tiles = all_tiles(mi_kmajor_rows(n_cols) / mi_tile_size(), tile_band());
+    std::vector<int32_t> tiles = all_tiles(mi_kmajor_rows(n_cols) / mi_tile_size(), tile_band(), row_done ? 1 : 0);
     int rc;
     if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
     MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
     (void)info;
-    return mi_gram_mi((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps,
-                      include_diagonal, out_kind, d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, ws.stream);
+    return launch_fused((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps, include_diagonal, out_kind,
+                        d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, row_done, ws.stream);
 }
 
 }  // namespace
@@ -364,6 +385,15 @@ int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, in
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld,
                int mode, double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
                const int32_t* d_tiles, int64_t n_tiles, void* stream) {
+    return launch_fused(d_kmajor, d_colstat, n_rows, n_cols, ld, mode, epsilon, include_diagonal, out_kind, d_out,
+                        ld_out, d_tiles, n_tiles, nullptr, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
+                 double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const int32_t* d_tiles,
+                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream) {
     int rc = check_shape(n_rows, n_cols);
     if (rc) return rc;
     if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
@@ -395,6 +425,7 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
     p.prefetch_dist = prefetch_dist();
     p.l2_hint = l2_hint();
     p.debug = tuning().debug;
+    p.row_done = row_done;
     p.trace = g_trace;
     fixed_point_consts(n_rows, &p.rcp, &p.off0);
     p.fix_s = xlogx_scale(n_rows);
@@ -404,9 +435,12 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
     p.table_thr = tuning().fixed == 0 ? -1 : tuning().fixed == 2 ? 0x7FFFFFFF : tuning().table_thr;
     int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
-    MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tuning().stages, tuning().epi_warps, tm, p, info.num_sms, (cudaStream_t)stream));
+    MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tuning().stages, tuning().epi_warps, tm, p, info.num_sms, stream));
     return MI_OK;
 }
+
+extern "C" {
+
 
 int mi_generate_words(uint64_t* d_words, int64_t n_rows, int64_t n_cols, uint64_t seed,
                       const uint64_t* d_col_threshold, const uint8_t* d_col_kind, const int32_t* d_col_src,
@@ -426,19 +460,75 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     if (out_kind == MI_OUT_COUNTS) return fail(MI_ERR_DOMAIN, "use mi_gram_ones_host for counts");
     if ((rc = check_padding(h_words, n_rows, n_cols))) return rc;
     std::lock_guard<std::mutex> lk(g_ws_mu);
+    const bool verbose = env_int("MI_B200_VERBOSE", 0) != 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto stamp = [&](const char* what) {
+        if (verbose)
+            fprintf(stderr, "[mi_all_pairs_host] %8.3f ms %s\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+    };
     Workspace* ws;
     DevInfo info;
     if ((rc = workspace_for(device, &ws, &info))) return rc;
     int64_t ld, m_pad;
     if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    stamp("H2D + unpack enqueued");
     const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
-    const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * esz;
-    if ((rc = ensure(&ws->out, &ws->out_cap, out_bytes))) return rc;
-    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out,
-                        n_cols, info)))
+    const size_t row_bytes = (size_t)n_cols * esz;
+    if ((rc = ensure(&ws->out, &ws->out_cap, row_bytes * (size_t)n_cols))) return rc;
+    // per-tile-row completion counters in pinned, mapped host memory
+    const int tile = mi_tile_size();
+    const int64_t T = m_pad / tile;
+    if (ws->row_done_cap < (size_t)T) {
+        if (ws->row_done_h) cudaFreeHost(ws->row_done_h);
+        ws->row_done_h = nullptr;
+        ws->row_done_cap = 0;
+        MI_CUDA(cudaHostAlloc((void**)&ws->row_done_h, (size_t)T * 4, cudaHostAllocMapped));
+        MI_CUDA(cudaHostGetDevicePointer((void**)&ws->row_done_d, ws->row_done_h, 0));
+        ws->row_done_cap = (size_t)T;
+        stamp("row counters allocated");
+    }
+    volatile unsigned int* done = ws->row_done_h;
+    for (int64_t I = 0; I < T; ++I) done[I] = 0;
+    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out, n_cols,
+                        info, ws->row_done_d)))
         return rc;
-    MI_CUDA(cudaMemcpyAsync(h_out, ws->out, out_bytes, cudaMemcpyDeviceToHost, ws->stream));
+    stamp("fused kernel enqueued");
+    // Stream finished rows to the host while the GEMM continues: rows of tile
+    // row b are final once every tile row I <= b is complete (its own tiles
+    // and all mirrors landing in it), so copy the completed prefix.
+    const unsigned cg = (unsigned)cta_group();
+    const int64_t min_chunk_rows = (int64_t)((16u << 20) / row_bytes) + 1;
+    int64_t copied = 0, I = 0;
+    bool kernel_done = false;
+    while (copied < n_cols) {
+        while (I < T && done[I] >= cg * (unsigned)(T - I)) ++I;
+        int64_t final_rows = I * tile < n_cols ? I * tile : n_cols;
+        if (kernel_done) final_rows = n_cols;
+        if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols)) {
+            MI_CUDA(cudaMemcpyAsync((char*)h_out + copied * row_bytes, (char*)ws->out + copied * row_bytes,
+                                    (size_t)(final_rows - copied) * row_bytes, cudaMemcpyDeviceToHost, ws->copy_stream));
+            if (verbose) {
+                char msg[96];
+                snprintf(msg, sizeof(msg), "D2H rows [%lld, %lld) issued", (long long)copied, (long long)final_rows);
+                stamp(msg);
+            }
+            copied = final_rows;
+            continue;
+        }
+        const cudaError_t q = cudaStreamQuery(ws->stream);
+        if (q == cudaSuccess) {
+            kernel_done = true;  // everything is final now
+        } else if (q != cudaErrorNotReady) {
+            cudaStreamSynchronize(ws->copy_stream);
+            return cuda_fail(q, "fused kernel");
+        } else {
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+    MI_CUDA(cudaStreamSynchronize(ws->copy_stream));
     MI_CUDA(cudaStreamSynchronize(ws->stream));
+    stamp("done");
     return MI_OK;
 }
 

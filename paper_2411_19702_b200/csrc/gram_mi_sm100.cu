@@ -495,6 +495,12 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            if (p.row_done) {
+                // publish: this CTA's rows and mirrors of tile (I, J) are in memory
+                __threadfence_system();
+                named_barrier_sync(3, EW * 32);
+                if (etid == 0) atomicAdd_system(p.row_done + tile.x, 1u);
+            }
             if (++acc == 2) { acc = 0; aph ^= 1u; }
         }
     }

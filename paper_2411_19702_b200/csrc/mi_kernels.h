@@ -36,6 +36,8 @@ struct GramMiParams {
     const long long* xlogx; // exact mode: fixed-point T(c) = c log2(c) 2^s, c = 0..N (or nullptr)
     const int2* blkrange;   // exact mode: (min, max) column sum per 128-column block
     int table_thr;          // table path when the tile's two column-sum ranges sum to <= this
+    unsigned int* row_done; // optional: per tile row I, +1 per CTA when its part of tile (I, J) is
+                            // stored (system scope; lets the host stream finished rows to host)
 };
 constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
 

@@ -197,15 +197,32 @@ class MIEngine:
 
     def all_pairs_host(self, words: np.ndarray | torch.Tensor, n_rows: int, n_cols: int, cfg=None,
                        out_dtype: torch.dtype = torch.float64, host_out: torch.Tensor | None = None) -> torch.Tensor:
-        """Host words in, host MI out (pinned tensor); H2D and D2H included."""
-        if isinstance(words, np.ndarray):
-            words = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))
-        words_dev = words.to(self.device, non_blocking=words.is_pinned())
-        dev_out = self.all_pairs_device(words_dev, n_rows, n_cols, cfg, out_dtype)
+        """Host words in, host MI out, through the C ABI's mi_all_pairs_host:
+        H2D, kernel 1, the fused kernel, and a D2H of finished row bands that
+        overlaps the GEMM.  ``host_out`` should be pinned for full PCIe speed."""
+        mode, eps, diag = _config_fields(cfg)
+        if out_dtype not in (torch.float64, torch.float32):
+            raise DomainError(f"out_dtype must be float64 or float32, got {out_dtype}")
+        if isinstance(words, torch.Tensor):
+            if words.device.type != "cpu" or not words.is_contiguous() or words.element_size() != 8:
+                raise DimensionError("host words must be a contiguous 64-bit CPU tensor")
+            if tuple(words.shape) != (n_cols, n_words(n_rows)):
+                raise DimensionError(f"words must have shape {(n_cols, n_words(n_rows))}")
+            wptr, keep = words.data_ptr(), words
+        else:
+            keep = np.ascontiguousarray(words)
+            if keep.dtype != np.uint64 or keep.shape != (n_cols, n_words(n_rows)):
+                raise DimensionError(f"words must be uint64 with shape {(n_cols, n_words(n_rows))}")
+            wptr = keep.ctypes.data
         if host_out is None:
             host_out = torch.empty((n_cols, n_cols), dtype=out_dtype, pin_memory=True)
-        host_out.copy_(dev_out, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
+        if host_out.dtype != out_dtype or tuple(host_out.shape) != (n_cols, n_cols) or not host_out.is_contiguous() \
+                or host_out.device.type != "cpu":
+            raise DimensionError("host_out must be a contiguous (m, m) CPU tensor of out_dtype")
+        kind = nat.MI_OUT_F64 if out_dtype == torch.float64 else nat.MI_OUT_F32
+        nat.check(nat.lib().mi_all_pairs_host(wptr, n_rows, n_cols, mode, eps, diag, kind, host_out.data_ptr(),
+                                              self.device.index), "mi_all_pairs_host")
+        del keep
         return host_out
 
 
