@@ -9,12 +9,15 @@ ctypes releases the GIL for the duration of each call.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 from pathlib import Path
 
 from .errors import ConsistencyError, DimensionError, DomainError, MiMatrixError, NativeError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmimatrix_b200.so"
+if os.environ.get("MI_B200_LIB"):  # experiments: A/B another build of the library
+    LIB_PATH = Path(os.environ["MI_B200_LIB"]).resolve()
 HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "mimatrix_b200.h"
 
 MI_OK = 0

@@ -198,10 +198,16 @@ int check_padding(const uint64_t* h_words, int64_t n_rows, int64_t n_cols) {
     return MI_OK;
 }
 
+// Tile rows/columns that contain real columns (the operand is padded to 256).
+int64_t tiles_per_side(int64_t n_cols) {
+    const int64_t t = mi_tile_size();
+    return (n_cols + t - 1) / t;
+}
+
 // Banded upper-triangle order: within a band of `band` tile rows, sweep J and
 // then the band's rows, so tiles that run concurrently share operand blocks.
 // `first` > 0 makes the first band that many rows (1 for the host path: tile
-// row 0 then completes in the first wave and the D2H of finished rows starts).
+// row 0 completes in the first wave, so the D2H of finished rows starts early).
 std::vector<int32_t> all_tiles(int64_t T, int band, int first = 0) {
     std::vector<int32_t> v;
     v.reserve((size_t)(T * (T + 1)));
@@ -301,7 +307,7 @@ int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t
               unsigned int* row_done = nullptr) {
     (void)m_pad;
     const int64_t n_tiles = mi_num_tiles(n_cols);
-    std::vector<int32_t> tiles = all_tiles(mi_kmajor_rows(n_cols) / mi_tile_size(), tile_band(), row_done ? 1 : 0);
+    std::vector<int32_t> tiles = all_tiles(tiles_per_side(n_cols), tile_band(), row_done ? 1 : 0);
     int rc;
     if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
     MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
@@ -341,7 +347,7 @@ int64_t mi_colstat_bytes(int64_t n_rows, int64_t n_cols) {
 int mi_tile_size(void) { return gram_mi_tile_size(cta_group()); }
 
 int64_t mi_num_tiles(int64_t n_cols) {
-    const int64_t T = mi_kmajor_rows(n_cols) / mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
     return T * (T + 1) / 2;
 }
 
@@ -350,7 +356,7 @@ int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* til
     if (world < 1 || rank < 0 || rank >= world)
         return -fail(MI_ERR_DOMAIN, "bad rank %d of world %d", rank, world);
     if (band <= 0) band = tile_band();
-    const int64_t T = mi_kmajor_rows(n_cols) / mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
     std::vector<int32_t> all = all_tiles(T, band);
     const int64_t total = (int64_t)all.size() / 2;
     int64_t count = 0;
@@ -478,7 +484,7 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     if ((rc = ensure(&ws->out, &ws->out_cap, row_bytes * (size_t)n_cols))) return rc;
     // per-tile-row completion counters in pinned, mapped host memory
     const int tile = mi_tile_size();
-    const int64_t T = m_pad / tile;
+    const int64_t T = tiles_per_side(n_cols);
     if (ws->row_done_cap < (size_t)T) {
         if (ws->row_done_h) cudaFreeHost(ws->row_done_h);
         ws->row_done_h = nullptr;
