@@ -222,10 +222,17 @@ def main():
     from paper_2411_19702_b200 import dispatch as dsp
 
     rank, world, local = dist_env()
+    # MI_B200_DIST_BACKEND=gloo (with ranks sharing GPUs) only exercises the
+    # multi-rank code path on fewer GPUs; timings are meaningless then.
+    backend = os.environ.get("MI_B200_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     eng = MIEngine.get(local)
 
     rec = datagen.config_recipe(args.config)
@@ -355,14 +362,15 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
     host_words = words_dev.cpu().pin_memory() if rank == 0 else None
     host_out = torch.empty((m, m), dtype=out_dtype, pin_memory=True) if rank == 0 else None
     steps = max(1, min(args.steps, 20))
+    shard_buf = torch.empty((m, m), dtype=out_dtype, device=dev) if world > 1 else None
 
     def once():
         if world == 1:
             eng.all_pairs_host(host_words, n, m, cfg, out_dtype, host_out=host_out)
         else:
             w = host_words.to(dev, non_blocking=True) if rank == 0 else None
-            local, tiles = dsp.mi_all_pairs_sharded(eng, w, n, m, cfg, out_dtype)
-            full = dsp.gather_to_root(local, m, tiles)
+            local, _ = dsp.mi_all_pairs_sharded(eng, w, n, m, cfg, out_dtype, out=shard_buf, zero_fill=True)
+            full = dsp.gather_to_root(local, m)
             if rank == 0:
                 host_out.copy_(full, non_blocking=True)
             stream.synchronize()

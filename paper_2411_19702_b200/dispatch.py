@@ -80,32 +80,37 @@ def run_sharded(words: torch.Tensor | None, n_rows: int, n_cols: int,
     return tiles
 
 
-def gather_to_root(out: torch.Tensor, n_cols: int, tiles: np.ndarray, root: int = 0, group=None) -> torch.Tensor | None:
-    """Assemble the full matrix on `root` from every rank's tiles.
+def gather_to_root(out: torch.Tensor, n_cols: int, root: int = 0, group=None) -> torch.Tensor | None:
+    """Assemble the full matrix on `root` from every rank's shard.
 
-    Each rank zeroes what it did not write and the shards are summed onto the
-    root; every element is written by exactly one rank, so the sum is an exact
-    gather (x + 0 == x in IEEE arithmetic).
+    ``out`` must be zero outside this rank's tiles and mirrors (allocate it
+    with ``zero_fill=True``).  Every element is written by exactly one rank, so
+    the sum-reduce onto the root is an exact gather (x + 0 == x in IEEE
+    arithmetic).
     """
     rank, world = world_info(group)
     if world == 1:
         return out
-    mask = torch.from_numpy(tile_mask(n_cols, tiles)).to(out.device)
-    shard = torch.where(mask, out[:n_cols, :n_cols], torch.zeros((), dtype=out.dtype, device=out.device))
+    shard = out[:n_cols, :n_cols]
+    if not shard.is_contiguous():
+        shard = shard.contiguous()
     dist.reduce(shard, dst=root, op=dist.ReduceOp.SUM, group=group)
     return shard if rank == root else None
 
 
 def mi_all_pairs_sharded(engine, words: torch.Tensor | None, n_rows: int, n_cols: int, cfg=None,
                          out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
-                         group=None) -> tuple[torch.Tensor, np.ndarray]:
+                         group=None, zero_fill: bool = False) -> tuple[torch.Tensor, np.ndarray]:
     """GPU version: broadcast + unpack + fused Gram/MI over this rank's tiles.
 
     Returns (local output with this rank's tiles and mirrors written, tiles).
+    ``zero_fill`` zeroes the rest of the local output, as gather_to_root needs.
     """
     rank, world = world_info(group)
     if out is None:
-        out = torch.empty((n_cols, n_cols), dtype=out_dtype, device=engine.device)
+        out = (torch.zeros if zero_fill else torch.empty)((n_cols, n_cols), dtype=out_dtype, device=engine.device)
+    elif zero_fill:
+        out.zero_()
 
     def compute(w, tiles, o):
         prep = engine.prepare(w, n_rows, n_cols)

@@ -62,7 +62,7 @@ def _worker(rank, world, port, n, m, result_q):
             words = torch.from_numpy(O.pack_bits(bits).view(np.int64))
         out = torch.zeros((m, m), dtype=torch.float64)
         tiles = dispatch.run_sharded(words, n, m, _oracle_compute(n, m), out, torch.device("cpu"))
-        full = dispatch.gather_to_root(out, m, tiles)
+        full = dispatch.gather_to_root(out, m)
         if rank == 0:
             ref = O.c_mi_all_pairs(words.numpy().view(np.uint64), n)
             result_q.put(("ok", bool(np.array_equal(full.numpy(), ref)), len(tiles)))
