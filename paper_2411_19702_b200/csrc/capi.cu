@@ -56,13 +56,14 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
                        env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8),
                        env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
-                       env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096)};
+                       env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
+                       env_int("MI_B200_PACE", -1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -71,6 +72,38 @@ int l2_hint() { return tuning().l2_hint; }
 int tile_band() { return tuning().band > 0 ? tuning().band : 8; }
 
 long long* g_trace = nullptr;  // experiments only (mi_debug_set_trace)
+
+// Per-device pacing slots of the fused kernel (kPaceMaxClusters x 32 B),
+// allocated once and initialised to "finished" (0xFF bytes).
+std::mutex g_pace_mu;
+unsigned int* g_pace[64] = {};
+
+// L2 pacing window in k-blocks (tuning "pace": -1 auto, 0 off, > 0 window).
+// Auto paces long runs -- many tile rounds or long K -- where the pairs drift
+// apart and the L2 stops sharing their operand reads (r01 sweep:
+// config 5 175 -> 108 ms, config 4 45.5 -> 40.3 ms); short runs (config 3,
+// 12 rounds) only pay the waits.
+int pace_window(int64_t n_tiles, int nkb, int num_sms) {
+    const int t = tuning().pace;
+    if (t >= 0) return t;
+    const int clusters = num_sms / 2;
+    const int64_t rounds = (n_tiles + clusters - 1) / clusters;
+    return (rounds > 16 || nkb > 2048) ? 32 : 0;
+}
+
+int pace_slots(int device, unsigned int** out) {
+    std::lock_guard<std::mutex> lk(g_pace_mu);
+    if (!g_pace[device]) {
+        const size_t bytes = (size_t)kPaceMaxClusters * kPaceStride * 4;
+        unsigned int* p = nullptr;
+        MI_CUDA(cudaMalloc((void**)&p, bytes));
+        MI_CUDA(cudaMemset(p, 0xFF, bytes));
+        MI_CUDA(cudaDeviceSynchronize());
+        g_pace[device] = p;
+    }
+    *out = g_pace[device];
+    return MI_OK;
+}
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -433,6 +466,13 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.debug = tuning().debug;
     p.row_done = row_done;
     p.trace = g_trace;
+    p.pace = nullptr;
+    p.pace_window = pace_window(n_tiles, p.num_k_blocks, info.num_sms);
+    if (p.pace_window > 0) {
+        int dev = 0;
+        MI_CUDA(cudaGetDevice(&dev));
+        if ((rc = pace_slots(dev, &p.pace))) return rc;
+    }
     fixed_point_consts(n_rows, &p.rcp, &p.off0);
     p.fix_s = xlogx_scale(n_rows);
     p.xlogx = xlogx_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
@@ -599,6 +639,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "fixed")) {
         if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "fixed must be 0, 1 or 2");
         t.fixed = value;
+    } else if (!strcmp(key, "pace")) {
+        if (value < -1) return fail(MI_ERR_DOMAIN, "pace must be -1 (auto), 0 (off) or a window in k-blocks");
+        t.pace = value;
     } else if (!strcmp(key, "epi_warps")) {
         if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");
         t.epi_warps = value;
@@ -619,6 +662,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "epi_warps")) return t.epi_warps;
     if (!strcmp(key, "fixed")) return t.fixed;
     if (!strcmp(key, "table_thr")) return t.table_thr;
+    if (!strcmp(key, "pace")) return t.pace;
     return -1;
 }
 

@@ -20,6 +20,8 @@
 //   warp 0            TMA producer (one lane): A = X[rows of I], B = X[rows of J]
 //   warp 1            TMEM allocator; then MMA issuer (one lane, leader CTA)
 //   warps 2 .. 2+E-1  epilogue (E = 8 or 16): tcgen05.ld -> counts -> MI -> global
+//   warp 2+E          pacer (leader CTA, when pacing is on): publishes this
+//                     pair's k-block progress and the minimum over all pairs
 // CG == 2: a CTA pair (cluster of 2) computes a 256x256 tile with
 // tcgen05.mma.cta_group::2 (M=256, N=256); each CTA stages half of A and half
 // of B, and owns 128 accumulator rows.  CG == 1: 128x128 tiles on one SM.
@@ -47,7 +49,8 @@ struct Cfg {
     static constexpr int ACC_COLS = MMA_N;          // TMEM columns per accumulator
     static constexpr int TMEM_COLS = 2 * ACC_COLS;  // double-buffered
     static constexpr int EPI_WARPS = EW;
-    static constexpr int THREADS = 32 * (kEpiWarp0 + EW);
+    static constexpr int PACER_WARP = kEpiWarp0 + EW;
+    static constexpr int THREADS = 32 * (kEpiWarp0 + EW);   // + one pacer warp when pacing
     static constexpr int COL_PARTS = EW / 4;        // epilogue warps per TMEM lane quadrant
     static constexpr int WARP_COLS = ACC_COLS / COL_PARTS;
     static constexpr uint32_t STAGE_TX = CG * 2 * kStageHalfBytes;  // bytes landing per stage
@@ -72,8 +75,9 @@ struct SmemLayout {
     static constexpr uint32_t tab_off = 2 * ST * kStageHalfBytes;  // log tables
     static constexpr uint32_t col_off = tab_off + TABB;            // column stats [2][TS]
     static constexpr uint32_t bar_off = col_off + 2 * 128 * CG * CSZ;
-    // full[ST], empty[ST], tfull[2], tempty[2], tmem slot
-    static constexpr uint32_t bytes = bar_off + (2 * ST + 4) * 8 + 16;
+    // full[ST], empty[ST], tfull[2], tempty[2], tmem slot, pacing words
+    static constexpr uint32_t pace_off = bar_off + (2 * ST + 4) * 8 + 8;
+    static constexpr uint32_t bytes = pace_off + 16;
     // + alignment slack when it fits (the dynamic window is normally 1 KB aligned)
     static constexpr uint32_t request = bytes + 1024 <= kMaxSmem ? bytes + 1024 : kMaxSmem;
     static_assert(bytes <= kMaxSmem, "pipeline does not fit in shared memory");
@@ -275,8 +279,8 @@ struct TileWalk {
     }
 };
 
-template <int CG, int OUT, int MODE, int ST, int EW>
-__global__ void __launch_bounds__(Cfg<CG, EW>::THREADS, 1)
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE>
+__global__ void __launch_bounds__(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1)
 gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p) {
     using C = Cfg<CG, EW>;
     using T = typename OutT<OUT>::T;
@@ -298,6 +302,9 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * ST + 2 + a); };
     const uint32_t tmem_slot = bar0 + 8u * (2 * ST + 4);
     volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(smem + L::bar_off + 8 * (2 * ST + 4));
+    // pacing words: [0] k-blocks issued by this pair's leader producer, [1] minimum
+    // over all pairs (written by the pacer warp), [2] producer finished
+    volatile uint32_t* s_pace = reinterpret_cast<volatile uint32_t*>(smem + L::pace_off);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
@@ -317,6 +324,9 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             mbar_init(tempty_bar(a), CG * EW);
         }
         fence_mbarrier_init();
+        s_pace[0] = 0u;
+        s_pace[1] = 0u;
+        s_pace[2] = 0u;
     }
     const int etid = (int)threadIdx.x - kEpiWarp0 * 32;  // epilogue thread id (may be < 0)
     if (etid >= 0 && etid < 128) tab[etid] = kLog2TabInit[etid];
@@ -328,6 +338,12 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 
     const int nkb = p.num_k_blocks;
     const TileWalk walk{cluster, n_clusters, p.n_tiles, nkb};
+    // L2 pacing: every pair walks K at the same rate over tiles drawn from a few
+    // shared column blocks; kept within a window of one another, the pairs read
+    // the same k-slices of those blocks close together in time, so the L2 serves
+    // them once from HBM instead of once per pair (tall N overflows the L2).
+    // (a separate instantiation: the check costs ~5% in the producer loop of short-K shapes)
+    const bool pacing = PACE && p.pace != nullptr && p.pace_window > 0 && rank == 0 && n_clusters <= kPaceMaxClusters;
 
     if (warp == 0) {
         // ================= TMA producer =================
@@ -347,7 +363,20 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 tma_prefetch_3d(&tmap_x, 0, tile.y * C::TS + (int)rank * 128, kb);
             }
             int t, kb;
+            bool pace_on = pacing;
+            const long long win = p.pace_window;
             for (long long g = 0; walk.at(g, t, kb); ++g) {
+                if (PACE && pace_on && (g & 15) == 0) {
+                    s_pace[0] = (uint32_t)g;
+                    if (g > win) {
+                        // wait (bounded: pacing is only a hint) while the slowest pair is too far behind
+                        int spins = 0;
+                        while ((long long)s_pace[1] + win < g) {
+                            __nanosleep(64);
+                            if (++spins > 20000) { pace_on = false; break; }
+                        }
+                    }
+                }
                 const int2 tile = p.tiles[t];
                 const int rowA = tile.x * C::TS + (int)rank * 128;
                 const int rowB = tile.y * C::TS + (int)rank * 128;
@@ -364,6 +393,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
                 if (++s == ST) { s = 0; ph ^= 1u; }
             }
+            s_pace[2] = 1u;
             // drain: the last commit of every stage must land before exit
             for (int q = 0; q < ST; ++q) {
                 mbar_wait(empty_bar(s), ph ^ 1u);
@@ -401,6 +431,28 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 1] = clock64();
                 if (++acc == 2) { acc = 0; aph ^= 1u; }
             }
+        }
+    } else if (PACE && warp == C::PACER_WARP) {
+        // ================= pacer =================
+        if (pacing) {
+            volatile uint32_t* gp = p.pace;
+            if (lane == 0) gp[cluster * kPaceStride] = 0u;
+            uint32_t last = 0u;
+            for (;;) {
+                const uint32_t done = s_pace[2];
+                const uint32_t mine = s_pace[0];
+                if (lane == 0 && mine != last) {
+                    gp[cluster * kPaceStride] = mine;
+                    last = mine;
+                }
+                uint32_t v = 0xFFFFFFFFu;
+                for (int c = (int)lane; c < n_clusters; c += 32) v = min(v, gp[c * kPaceStride]);
+                v = __reduce_min_sync(0xFFFFFFFFu, v);
+                if (lane == 0) s_pace[1] = v;
+                if (done) break;
+                __nanosleep(256);
+            }
+            if (lane == 0) gp[cluster * kPaceStride] = 0xFFFFFFFFu;  // finished pairs never hold others back
         }
     } else {
         // ================= epilogue =================
@@ -515,9 +567,9 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 
 // ---------------------------------------------------------------- launch
 
-template <int CG, int OUT, int MODE, int ST, int EW>
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE>
 static cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream) {
-    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW>;
+    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW, PACE>;
     constexpr uint32_t smem = SmemLayout<CG, ST>::request;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -526,7 +578,7 @@ static cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, i
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG, 1, 1);
-    cfg.blockDim = dim3(Cfg<CG, EW>::THREADS, 1, 1);
+    cfg.blockDim = dim3(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -541,22 +593,35 @@ static cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, i
 
 cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,
                            const GramMiParams& p, int num_sms, cudaStream_t stream) {
-#define MI_DISPATCH(CGV, OV, MV, STV, EWV)                                                       \
-    if (cg == CGV && out_kind == OV && mode == MV && stages == STV && epi_warps == EWV) \
-        return launch_impl<CGV, OV, MV, STV, EWV>(tmap, p, num_sms, stream);
+    const bool pace = p.pace != nullptr && p.pace_window > 0;
+#define MI_DISPATCH_P(CGV, OV, MV, STV, EWV, PV)                                                               \
+    if (cg == CGV && out_kind == OV && mode == MV && stages == STV && epi_warps == EWV && pace == PV) \
+        return launch_impl<CGV, OV, MV, STV, EWV, PV>(tmap, p, num_sms, stream);
+#define MI_DISPATCH(CGV, OV, MV, STV, EWV) MI_DISPATCH_P(CGV, OV, MV, STV, EWV, false)
     MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EXACT, 6, 8)
     MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EPSILON, 6, 8)
     MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8)
     MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EPSILON, 6, 8)
     MI_DISPATCH(2, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
+    MI_DISPATCH_P(2, MI_OUT_F64, MI_MODE_EXACT, 6, 8, true)
+    MI_DISPATCH_P(2, MI_OUT_F64, MI_MODE_EPSILON, 6, 8, true)
+    MI_DISPATCH_P(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8, true)
+    MI_DISPATCH_P(2, MI_OUT_F32, MI_MODE_EPSILON, 6, 8, true)
+    MI_DISPATCH_P(2, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8, true)
     MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EXACT, 6, 8)
     MI_DISPATCH(1, MI_OUT_F64, MI_MODE_EPSILON, 6, 8)
     MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EXACT, 6, 8)
     MI_DISPATCH(1, MI_OUT_F32, MI_MODE_EPSILON, 6, 8)
     MI_DISPATCH(1, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
 #undef MI_DISPATCH
+#undef MI_DISPATCH_P
     // knob combinations without a dedicated build fall back to the default build of the variant
     if (stages != 6 || epi_warps != 8) return launch_gram_mi(cg, out_kind, mode, 6, 8, tmap, p, num_sms, stream);
+    if (pace) {  // no paced build of this variant (CG == 1)
+        GramMiParams q = p;
+        q.pace = nullptr;
+        return launch_gram_mi(cg, out_kind, mode, stages, epi_warps, tmap, q, num_sms, stream);
+    }
     return cudaErrorInvalidValue;
 }
 

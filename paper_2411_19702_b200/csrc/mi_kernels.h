@@ -38,7 +38,11 @@ struct GramMiParams {
     int table_thr;          // table path when the tile's two column-sum ranges sum to <= this
     unsigned int* row_done; // optional: per tile row I, +1 per CTA when its part of tile (I, J) is
                             // stored (system scope; lets the host stream finished rows to host)
+    unsigned int* pace;     // optional: per-cluster k-block progress, stride kPaceStride (L2 pacing)
+    int pace_window;        // leader producers stay within this many k-blocks of the slowest pair (0 = off)
 };
+constexpr int kPaceStride = 8;          // u32 per cluster slot (one 32-B sector each)
+constexpr int kPaceMaxClusters = 256;
 constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
 
 cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,

@@ -129,7 +129,8 @@ class MIEngine:
         return int(L.mi_kmajor_ld(n_rows)), int(L.mi_kmajor_rows(n_cols))
 
     def tiles(self, n_cols: int, rank: int = 0, world: int = 1) -> torch.Tensor:
-        key = (n_cols, rank, world)
+        # the list depends on the tile size (cta_group) and order (band) knobs
+        key = (n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("band"))
         t = self._tiles.get(key)
         if t is None:
             host = nat.tile_list(n_cols, rank, world)

@@ -142,6 +142,36 @@ def test_edge_shapes_counts_and_mi(engine, n, m, density):
     assert float(np.max(np.abs(mi - ref))) < TOL_F64
 
 
+KNOB_VARIANTS = [
+    {"pace": 0}, {"pace": 1}, {"pace": 16}, {"pace": 100000}, {"cta_group": 1}, {"cta_group": 1, "pace": 16},
+    {"fixed": 0}, {"fixed": 2}, {"band": 1}, {"band": 3}, {"l2_hint": 0}, {"prefetch": 4},
+]
+
+
+@pytest.mark.parametrize("knobs", KNOB_VARIANTS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()))
+def test_tuning_variants_agree(engine, knobs):
+    """Every tuning knob (tile size, L2 pacing, epilogue path, tile order, L2
+    hints) changes the schedule only: counts stay bit-exact and MI within the
+    float64 tolerance of the oracle."""
+    from paper_2411_19702_b200 import _native as nat
+
+    rng = np.random.default_rng(4242)
+    n, m = 20_000, 1_100
+    bits = rand_bits(rng, n, m, 0.3)
+    words = O.pack_bits(bits)
+    old = {k: nat.get_tuning(k) for k in knobs}
+    try:
+        nat.set_tuning(**knobs)
+        g, v = gpu_counts(engine, words, n)
+        mi = gpu_mi(engine, words, n)
+    finally:
+        nat.set_tuning(**old)
+    assert np.array_equal(g, O.c_gram_ones(words))
+    ref = O.c_mi_all_pairs(words, n)
+    assert np.array_equal(mi, mi.T)
+    assert float(np.max(np.abs(mi - ref))) < TOL_F64
+
+
 def test_determinism_and_c_abi_host_path(engine):
     from paper_2411_19702_b200 import BinaryMatrix, mi_all_pairs, mi_all_pairs_c_abi
 
