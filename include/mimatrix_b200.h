@@ -113,7 +113,9 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
  * epilogue warps), "fixed" (exact-mode epilogue: 1 adaptive per tile, default;
  * 0 FP64 only; 2 fixed-point table only), "table_thr" (adaptive threshold on
  * the tile's column-sum spread), "pace" (L2 pacing window in k-blocks that
- * keeps the SM pairs' K sweeps together: -1 auto (default), 0 off).  Also
+ * keeps the SM pairs' K sweeps together: -1 auto (default), 0 off), "tail"
+ * (the last partial round of tiles split over the idle SM pairs: 1 auto,
+ * default; 0 off; 2 column slices; 3 K ranges).  Also
  * settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */

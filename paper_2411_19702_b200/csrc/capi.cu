@@ -56,14 +56,14 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
                        env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8),
                        env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
-                       env_int("MI_B200_PACE", -1)};
+                       env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -89,6 +89,63 @@ int pace_window(int64_t n_tiles, int nkb, int num_sms) {
     const int clusters = num_sms / 2;
     const int64_t rounds = (n_tiles + clusters - 1) / clusters;
     return (rounds > 16 || nkb > 2048) ? 32 : 0;
+}
+
+// Tail split of the last partial round (GramMiParams::tail_*): its r tiles
+// become s units each so that r * s of the clusters share it instead of r.
+// Short K (< kTailKMinKb k-blocks; latency-bound): column slices of the tile
+// with the full K range, s a power of two, slices >= 32 wide.  Long K (the
+// slices would be load-bound: a narrow MMA still streams a full A block):
+// K ranges of the full tile, s = clusters / r, whose int32 partials are summed
+// by e <= s epilogue units, one column slice each (config 3: 820 tiles = 11
+// rounds of 74 + 6; the 6 run as 72 K ranges, summed by 48 epilogue slices).
+// Knob "tail": 0 off, 1 auto, 2 slices only, 3 K ranges only.
+constexpr int kTailKMinKb = 256;
+struct TailPlan {
+    int n_full, split, kmode, epi;
+};
+TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb) {
+    TailPlan tp{(int)n_tiles, 1, 0, 1};
+    const int mode = tuning().tail;
+    if (!mode || clusters < 2) return tp;
+    const int64_t r = n_tiles % clusters;
+    if (r == 0) return tp;
+    const bool kmode = mode == 3 || (mode == 1 && nkb >= kTailKMinKb);
+    int s = 1, e = 1;
+    while (e * 2 * 32 <= 128 * cg && r * e * 2 <= clusters) e *= 2;  // power-of-two column slices
+    if (kmode) {
+        s = (int)(clusters / r);
+        if (s > nkb) s = nkb;
+        if (s > kTailMaxUnits) s = kTailMaxUnits;
+        while (e > s) e /= 2;  // epilogue slices stay a power of two
+    } else {
+        s = e;
+    }
+    if (s < 2 || r * s > kTailMaxUnits) return tp;
+    tp.n_full = (int)(n_tiles - r);
+    tp.split = s;
+    tp.kmode = kmode ? 1 : 0;
+    tp.epi = kmode ? e : s;
+    return tp;
+}
+
+std::mutex g_tail_mu;
+unsigned int* g_tail_flag[64] = {};
+uint32_t* g_tail_part[64] = {};
+
+int tail_slots(int device, unsigned int** flag, uint32_t** part) {
+    std::lock_guard<std::mutex> lk(g_tail_mu);
+    if (!g_tail_flag[device]) {
+        unsigned int* f = nullptr;
+        uint32_t* q = nullptr;
+        MI_CUDA(cudaMalloc((void**)&f, (size_t)kTailMaxUnits * 2 * 4));
+        MI_CUDA(cudaMalloc((void**)&q, (size_t)kTailMaxUnits * 128 * 256 * 4));
+        g_tail_flag[device] = f;
+        g_tail_part[device] = q;
+    }
+    *flag = g_tail_flag[device];
+    *part = g_tail_part[device];
+    return MI_OK;
 }
 
 int pace_slots(int device, unsigned int** out) {
@@ -466,12 +523,21 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.debug = tuning().debug;
     p.row_done = row_done;
     p.trace = g_trace;
+    int dev = 0;
+    MI_CUDA(cudaGetDevice(&dev));
     p.pace = nullptr;
     p.pace_window = pace_window(n_tiles, p.num_k_blocks, info.num_sms);
-    if (p.pace_window > 0) {
-        int dev = 0;
-        MI_CUDA(cudaGetDevice(&dev));
-        if ((rc = pace_slots(dev, &p.pace))) return rc;
+    if (p.pace_window > 0 && (rc = pace_slots(dev, &p.pace))) return rc;
+    const TailPlan tp = tail_plan(n_tiles, cta_group(), info.num_sms / cta_group(), p.num_k_blocks);
+    p.n_full = tp.n_full;
+    p.tail_split = tp.split;
+    p.tail_kmode = tp.kmode;
+    p.tail_epi = tp.epi;
+    p.tail_flag = nullptr;
+    p.tail_part = nullptr;
+    if (tp.kmode) {
+        if ((rc = tail_slots(dev, &p.tail_flag, &p.tail_part))) return rc;
+        MI_CUDA(cudaMemsetAsync(p.tail_flag, 0, (size_t)(n_tiles - tp.n_full) * 2 * 4, stream));
     }
     fixed_point_consts(n_rows, &p.rcp, &p.off0);
     p.fix_s = xlogx_scale(n_rows);
@@ -536,6 +602,17 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     }
     volatile unsigned int* done = ws->row_done_h;
     for (int64_t I = 0; I < T; ++I) done[I] = 0;
+    // completion count of tile row I: +1 per CTA per tile (I, J), or per
+    // column slice of a split tail tile -- the same tile list and tail plan
+    // that run_fused launches
+    const unsigned cg = (unsigned)cta_group();
+    std::vector<unsigned> expect((size_t)T, 0u);
+    {
+        const std::vector<int32_t> tl = all_tiles(T, tile_band(), 1);
+        const int64_t nt = (int64_t)tl.size() / 2;
+        const TailPlan tp = tail_plan(nt, (int)cg, info.num_sms / (int)cg, (int)(mi_kmajor_ld(n_rows) / 128));
+        for (int64_t k = 0; k < nt; ++k) expect[(size_t)tl[2 * k]] += cg * (k >= tp.n_full ? (unsigned)tp.epi : 1u);
+    }
     if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out, n_cols,
                         info, ws->row_done_d)))
         return rc;
@@ -543,12 +620,11 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     // Stream finished rows to the host while the GEMM continues: rows of tile
     // row b are final once every tile row I <= b is complete (its own tiles
     // and all mirrors landing in it), so copy the completed prefix.
-    const unsigned cg = (unsigned)cta_group();
     const int64_t min_chunk_rows = (int64_t)((16u << 20) / row_bytes) + 1;
     int64_t copied = 0, I = 0;
     bool kernel_done = false;
     while (copied < n_cols) {
-        while (I < T && done[I] >= cg * (unsigned)(T - I)) ++I;
+        while (I < T && done[I] >= expect[(size_t)I]) ++I;
         int64_t final_rows = I * tile < n_cols ? I * tile : n_cols;
         if (kernel_done) final_rows = n_cols;
         if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols)) {
@@ -639,6 +715,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "fixed")) {
         if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "fixed must be 0, 1 or 2");
         t.fixed = value;
+    } else if (!strcmp(key, "tail")) {
+        if (value < 0 || value > 3) return fail(MI_ERR_DOMAIN, "tail must be 0 (off), 1 (auto), 2 (slices) or 3 (K ranges)");
+        t.tail = value;
     } else if (!strcmp(key, "pace")) {
         if (value < -1) return fail(MI_ERR_DOMAIN, "pace must be -1 (auto), 0 (off) or a window in k-blocks");
         t.pace = value;
@@ -663,11 +742,14 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "fixed")) return t.fixed;
     if (!strcmp(key, "table_thr")) return t.table_thr;
     if (!strcmp(key, "pace")) return t.pace;
+    if (!strcmp(key, "tail")) return t.tail;
     return -1;
 }
 
 // Not part of the public header: route per-tile timestamps of cluster 0 into a
-// device buffer of 64 x 4 int64 (tools/trace_tiles.py), or nullptr to stop.
+// device buffer of 64 x 4 int64 (tools/trace_tiles.py) followed by 256 x 4
+// per-cluster globaltimer stamps (start, main tiles done, tail done), or
+// nullptr to stop.
 void mi_debug_set_trace(void* d_buf) { g_trace = reinterpret_cast<long long*>(d_buf); }
 
 void mi_release_workspace(void) {

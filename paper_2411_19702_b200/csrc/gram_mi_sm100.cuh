@@ -1,0 +1,740 @@
+// Kernel template of the fused Gram + MI path (instantiated by gram_mi_inst_*.cu).
+#pragma once
+// Kernel 2+3: symmetric upper-triangle int8 Gram on tcgen05 with the mutual-
+// information epilogue fused onto the TMEM accumulators.
+//
+// Replaces, for one output tile at a time, the reference's
+//   _kernels.gram_ones_kernel        _kernels.py:48-61   (G11 = D^T D by AND+popcount)
+//   gram.gram_complete_optimized     gram.py:88-111      (g00 / g01 in closed form)
+//   engine.probabilities             engine.py:93-102
+//   engine.mi_from_probabilities     engine.py:116-141   (four cells, fixed order, mirror)
+// so that G never reaches HBM: each (I <= J) tile of G lives in TMEM, is read
+// once by the epilogue warps and written out as MI(I,J) and its mirror
+// MI(J,I).
+//
+// Layout: X is the K-major int8 expansion of the bit-packed
+// columns, X[c][r] = bit r of column c, stored k-blocked as
+// [N_pad/128][m_pad][128 bytes] (N_pad % 128 == 0, m_pad % 256 == 0, zero
+// padded) so each 128 x 128 TMA box is one contiguous 16 KB chunk.  Both GEMM
+// operands are row blocks of X.
+//
+// Warp roles (one CTA per SM, persistent over a static tile list):
+//   warp 0            TMA producer (one lane): A = X[rows of I], B = X[rows of J]
+//   warp 1            TMEM allocator; then MMA issuer (one lane, leader CTA)
+//   warps 2 .. 2+E-1  epilogue (E = 8 or 16): tcgen05.ld -> counts -> MI -> global
+//   warp 2+E          pacer (leader CTA, when pacing is on): publishes this
+//                     pair's k-block progress and the minimum over all pairs
+// CG == 2: a CTA pair (cluster of 2) computes a 256x256 tile with
+// tcgen05.mma.cta_group::2 (M=256, N=256); each CTA stages half of A and half
+// of B, and owns 128 accumulator rows.  CG == 1: 128x128 tiles on one SM.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <type_traits>
+
+#include "milog.cuh"
+#include "mi_kernels.h"
+#include "ptx.cuh"
+
+namespace mib200 {
+
+constexpr int kEpiWarp0 = 2;
+constexpr int kBK = 128;                    // K bytes per pipeline stage (= 128B swizzle span)
+constexpr int kStageHalfBytes = 128 * kBK;  // one 128-row operand half: 16 KB
+constexpr uint32_t kMaxSmem = 232448;       // 227 KB opt-in per CTA on sm_100
+
+template <int CG, int EW>
+struct Cfg {
+    static constexpr int TS = 128 * CG;             // square output tile
+    static constexpr int MMA_M = 128 * CG;
+    static constexpr int MMA_N = 128 * CG;
+    static constexpr int ACC_COLS = MMA_N;          // TMEM columns per accumulator
+    static constexpr int TMEM_COLS = 2 * ACC_COLS;  // double-buffered
+    static constexpr int EPI_WARPS = EW;
+    static constexpr int PACER_WARP = kEpiWarp0 + EW;
+    static constexpr int THREADS = 32 * (kEpiWarp0 + EW);   // + one pacer warp when pacing
+    static constexpr int COL_PARTS = EW / 4;        // epilogue warps per TMEM lane quadrant
+    static constexpr int WARP_COLS = ACC_COLS / COL_PARTS;
+    static constexpr uint32_t STAGE_TX = CG * 2 * kStageHalfBytes;  // bytes landing per stage
+    static_assert(EW % 4 == 0 && WARP_COLS % 16 == 0, "bad epilogue split");
+};
+
+// Per-tile column marginals staged in shared memory by the epilogue: the
+// FP64-path logs and the fixed-point (table path) term of each column.
+struct ColS {
+    double v, e1, e0, f1, f0;  // v, and log2 v = e1 + f1, log2 (N - v) = e0 + f0
+    long long q;               // T(v) + T(N - v)
+    int vi, pad;
+};
+constexpr uint32_t kTabBytes = 128u * 16u;  // log2_frac double2 table
+
+template <int CG, int ST>
+struct SmemLayout {
+    static constexpr uint32_t CSZ = (uint32_t)sizeof(ColS);
+    static constexpr uint32_t TABB = kTabBytes;
+    static constexpr uint32_t a_off = 0;
+    static constexpr uint32_t b_off = ST * kStageHalfBytes;
+    static constexpr uint32_t tab_off = 2 * ST * kStageHalfBytes;  // log tables
+    static constexpr uint32_t col_off = tab_off + TABB;            // column stats [2][TS]
+    static constexpr uint32_t bar_off = col_off + 2 * 128 * CG * CSZ;
+    // full[ST], empty[ST], tfull[2], tempty[2], tmem slot, pacing words
+    static constexpr uint32_t pace_off = bar_off + (2 * ST + 4) * 8 + 8;
+    static constexpr uint32_t bytes = pace_off + 16;
+    // + alignment slack when it fits (the dynamic window is normally 1 KB aligned)
+    static constexpr uint32_t request = bytes + 1024 <= kMaxSmem ? bytes + 1024 : kMaxSmem;
+    static_assert(bytes <= kMaxSmem, "pipeline does not fit in shared memory");
+};
+
+// ---------------------------------------------------------------- epilogue math
+//
+// Exact-mode MI of one pair (engine.py:105-109,116-141), from integer counts.
+// Each cell contributes c * log2(c N / (a b)), summed in the reference's fixed
+// order (1,1), (1,0), (0,1), (0,0) and divided by N at the end.  The log of the
+// ratio is assembled as integer exponents plus table-driven mantissa fractions
+// (milog.cuh): L = ((e_c + ((e_N - e_a) - e_b)) + (((f_c + f_N) - f_a) - f_b),
+// with the marginal logs precomputed once per column by kernel 1.  Identical
+// mantissas cancel exactly, so an identical balanced pair gives exactly 1.0 and
+// an independent one (c N == a b with equal mantissas) exactly 0.0, as in the
+// reference; elsewhere the result is within ~1e-15 of the reference's value.
+// All counts are exact integers held in doubles; no I2F conversions.
+
+struct RowMarg {        // the tile row's (A side) marginals
+    double v, nv;       // v_i, N - v_i
+    double er1, er0;    // e_N - e(v_i), e_N - e(N - v_i)
+    double f1, f0;
+};
+
+__device__ __forceinline__ RowMarg row_marg(const ColS& s, double eN, double dN) {
+    return RowMarg{s.v, dN - s.v, eN - s.e1, eN - s.e0, s.f1, s.f0};
+}
+__device__ __forceinline__ ColS col_s(const ColStat& s) { return ColS{s.v, s.e1, s.e0, s.f1, s.f0, s.q, s.vi, 0}; }
+
+// c * L for one cell; c == 0 contributes exactly 0 (0 * log 0 = 0).
+__device__ __forceinline__ double cell_term(double c, double eab, double fa, double fb, double fN,
+                                            const double2* __restrict__ tab) {
+    const double cs = c > 0.0 ? c : 1.0;
+    const int hi = __double2hiint(cs);
+    const int lo = __double2loint(cs);
+    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);  // mantissa in [1, 2)
+    const double2 t = tab[(hi >> 13) & 127];
+    const double u = fma(m, t.x, -1.0);
+    double p = fma(u, kLog2C8, kLog2C7);
+    p = fma(u, p, kLog2C6);
+    p = fma(u, p, kLog2C5);
+    p = fma(u, p, kLog2C4);
+    p = fma(u, p, kLog2C3);
+    p = fma(u, p, kLog2C2);
+    p = fma(u, p, kLog2C1);
+    const double fc = fma(u, p, t.y);                                         // log2(mantissa)
+    const double ec = u32_to_double((uint32_t)hi >> 20) - 1023.0;             // exponent, exact
+    const double L = (ec + eab) + (((fc + fN) - fa) - fb);
+    return __dmul_rn(c, L);  // explicit rounding: no FMA contraction with the running sum,
+}                            // so every call site (both diagonal orientations) agrees bitwise
+
+// s / N, correctly rounded: q = s * RN(1/N) refined by one exact-remainder step.
+__device__ __forceinline__ double div_n(double s, double dN, double rN) {
+    const double q = s * rN;
+    const double r = fma(-q, dN, s);
+    return fma(r, rN, q);
+}
+
+__device__ __forceinline__ double mi_exact(double g, const RowMarg& A, const ColS& B, double fN,
+                                           double dN, double rN, const double2* __restrict__ tab) {
+    const double c10 = A.v - g;
+    const double c01 = B.v - g;
+    const double c00 = (A.nv - B.v) + g;
+    double s = cell_term(g, A.er1 - B.e1, A.f1, B.f1, fN, tab);               // (1,1)
+    s = __dadd_rn(s, cell_term(c10, A.er1 - B.e0, A.f1, B.f0, fN, tab));      // (1,0)
+    s = __dadd_rn(s, cell_term(c01, A.er0 - B.e1, A.f0, B.f1, fN, tab));      // (0,1)
+    s = __dadd_rn(s, cell_term(c00, A.er0 - B.e0, A.f0, B.f0, fN, tab));      // (0,0)
+    return div_n(s, dN, rN);
+}
+
+// Epsilon mode (engine.py:112-113): p * log2((p + eps) / (e + eps)) with
+// p = count / n and e = (a / n)(b / n), evaluated with the reference's operations.
+__device__ __forceinline__ double mi_epsilon(double g, double vi, double vj, double dN, double eps) {
+    const double a1 = vi, a0 = dN - vi, b1 = vj, b0 = dN - vj;
+    const double pa1 = a1 / dN, pa0 = a0 / dN, pb1 = b1 / dN, pb0 = b0 / dN;
+    // explicit roundings (no FMA contraction), like the reference's NumPy ops
+    auto term = [&](double c, double pa, double pb) {
+        const double p = c / dN;
+        const double e = __dadd_rn(__dmul_rn(pa, pb), eps);
+        return __dmul_rn(p, log2(__dadd_rn(p, eps) / e));
+    };
+    double s = term(g, pa1, pb1);
+    s = __dadd_rn(s, term(vi - g, pa1, pb0));
+    s = __dadd_rn(s, term(vj - g, pa0, pb1));
+    s = __dadd_rn(s, term((dN - vi - vj) + g, pa0, pb0));
+    return s;
+}
+
+template <int OUT>
+struct OutT;
+template <> struct OutT<MI_OUT_COUNTS> { using T = int32_t; };
+template <> struct OutT<MI_OUT_F64> { using T = double; };
+template <> struct OutT<MI_OUT_F32> { using T = float; };
+
+__device__ __forceinline__ void store_pair(double* p, double a, double b) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ void store_pair(float* p, float a, float b) {
+    *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
+__device__ __forceinline__ void store_pair(int32_t* p, int32_t a, int32_t b) {
+    *reinterpret_cast<int2*>(p) = make_int2(a, b);
+}
+
+// The tile row's fixed-point marginals (table path).
+struct RowQ {
+    int v, nmv;      // v_i, N - v_i
+    long long kq;    // T(N) - (T(v_i) + T(N - v_i))
+};
+
+// 16 columns of one output row (this thread's TMEM lane): MI (or counts), the
+// coalesced mirror store of column i and the direct store of row i.
+// TABLE: exact mode through the fixed-point c log2 c table (integer sums, no
+// FP64 -- B200 runs FP64 on the tensor datapath, ~23x slower under tcgen05.mma);
+// otherwise the FP64 epilogue (epsilon mode, and exact-mode tiles whose column
+// sums are too spread out for the table gathers to stay in L1).
+template <int OUT, int MODE, bool DIAG, bool TABLE, typename T>
+__device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A, const RowQ& AQ,
+                                           const ColS* __restrict__ cols, const ColS& Arow,
+                                           const GramMiParams& p, double eN, double fN, double dN, double rN,
+                                           const double2* __restrict__ tab, T* __restrict__ out, int64_t ld,
+                                           bool row_ok, bool vec_ok) {
+    const int m = p.m;
+    // 1) all 16 values into registers first: independent chains (and table
+    //    gathers) the scheduler can overlap, no stores in between
+    T v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int j = j0 + k;
+        if constexpr (OUT == MI_OUT_COUNTS) {
+            v[k] = (T)r[k];
+        } else if constexpr (TABLE) {
+            // integer sum of fixed-point terms: exact and order-independent, so
+            // both halves of a diagonal tile agree bit for bit
+            const int g = (int)r[k];
+            const int bv = cols[k].vi;
+            const long long* __restrict__ X = p.xlogx;
+            const long long S = (__ldg(X + g) + __ldg(X + (AQ.v - g))) +
+                                (__ldg(X + (bv - g)) + __ldg(X + (AQ.nmv - bv + g))) + (AQ.kq - cols[k].q);
+            T x = fixed_to_fp<T>(S, p.rcp, p.off0);
+            if (DIAG && !p.include_diagonal && i == j) x = (T)0;
+            v[k] = x;
+        } else {
+            const double g = u32_to_double(r[k]);
+            const ColS& B = cols[k];
+            double x;
+            if constexpr (MODE == MI_MODE_EXACT) {
+                if (DIAG && j < i) {
+                    // (min, max) orientation: the two halves of a diagonal
+                    // tile are then bit-identical mirrors
+                    x = mi_exact(g, row_marg(B, eN, dN), Arow, fN, dN, rN, tab);
+                } else {
+                    x = mi_exact(g, A, B, fN, dN, rN, tab);
+                }
+            } else {
+                x = (DIAG && j < i) ? mi_epsilon(g, B.v, A.v, dN, p.eps) : mi_epsilon(g, A.v, B.v, dN, p.eps);
+            }
+            if (DIAG && !p.include_diagonal && i == j) x = 0.0;
+            v[k] = (T)x;
+        }
+    }
+    if (p.debug) {  // keep the math alive without storing the tile
+        T acc = v[0];
+#pragma unroll
+        for (int k = 1; k < 16; ++k) acc = acc + v[k];
+        if (acc == (T)-12345) out[0] = acc;
+        return;
+    }
+    if (!row_ok) return;
+    // 2) mirror tile: row j, column i (coalesced across the warp)
+    if (!DIAG) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (j0 + k < m) out[(int64_t)(j0 + k) * ld + i] = v[k];
+    }
+    // 3) direct tile: row i, columns j0 .. j0+15
+    T* dst = out + (int64_t)i * ld + j0;
+#pragma unroll
+    for (int k = 0; k < 16; k += 2) {
+        if (vec_ok && j0 + k + 1 < m) {
+            store_pair(dst + k, v[k], v[k + 1]);
+        } else {
+            if (j0 + k < m) dst[k] = v[k];
+            if (j0 + k + 1 < m) dst[k + 1] = v[k + 1];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- the kernel
+
+struct TileWalk {
+    // Linear walk over (my tile, k-block) pairs: step g -> tile index, k-block.
+    int cluster, n_clusters, n_tiles, nkb;
+    __device__ __forceinline__ bool at(long long g, int& t, int& kb) const {
+        const long long it = g / nkb;
+        t = cluster + (int)it * n_clusters;
+        kb = (int)(g - it * nkb);
+        return t < n_tiles;
+    }
+};
+
+// The split tail unit's producer and MMA loops live out of line: inlined after
+// the main loops they cost ~3% of the main loops' throughput (code layout).
+// Tail units (GramMiParams::tail_*): column slice c (rows of B from
+// J TS + c W + rank W / CG; the TMA box still moves 128 rows, the MMA reads the
+// first W / CG) over k-blocks [kb0, kb1), the full K range for slices.
+template <int CG, int ST>
+__device__ __noinline__ uint2 producer_tail(const CUtensorMap* tmap, int2 tile, uint32_t rank, int slice, int width,
+                                            int kb0, int kb1, uint32_t sA, uint32_t sB, uint32_t bar0,
+                                            uint64_t policy, int s, uint32_t ph) {
+    using C = Cfg<CG, 8>;
+    const int rowA = tile.x * C::TS + (int)rank * 128;
+    const int rowB = tile.y * C::TS + slice * width + (int)rank * (width / CG);
+    for (int kb = kb0; kb < kb1; ++kb) {
+        const uint32_t full = bar0 + 8u * s, empty = bar0 + 8u * (ST + s);
+        mbar_wait(empty, ph ^ 1u);
+        const uint32_t fb = (CG == 2) ? map_to_cta(full, 0u) : full;
+        if (rank == 0) mbar_arrive_expect_tx(full, C::STAGE_TX);
+        tma_load_3d<CG>(sA + s * kStageHalfBytes, tmap, fb, 0, rowA, kb, policy);
+        tma_load_3d<CG>(sB + s * kStageHalfBytes, tmap, fb, 0, rowB, kb, policy);
+        if (++s == ST) { s = 0; ph ^= 1u; }
+    }
+    return make_uint2((uint32_t)s, ph);
+}
+
+template <int CG, int ST>
+__device__ __noinline__ void mma_tail(uint32_t tmem_base, int width, int kb0, int kb1, uint32_t sA, uint32_t sB,
+                                      uint32_t bar0, int s, uint32_t ph, int acc, uint32_t aph) {
+    using C = Cfg<CG, 8>;
+    const uint32_t idesc = umma_idesc_i8(C::MMA_M, width);  // M x W accumulator in TMEM columns [0, W)
+    mbar_wait(bar0 + 8u * (2 * ST + 2 + acc), aph ^ 1u);  // tempty[acc]
+    tc_fence_after();
+    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+    for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(bar0 + 8u * s, ph);  // full[s]
+        tc_fence_after();
+        const uint64_t adesc = umma_desc_sw128_kmajor(sA + s * kStageHalfBytes);
+        const uint64_t bdesc = umma_desc_sw128_kmajor(sB + s * kStageHalfBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 32; ++k)
+            umma_i8<CG>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+        umma_commit<CG>(bar0 + 8u * (ST + s));  // empty[s]
+        if (++s == ST) { s = 0; ph ^= 1u; }
+    }
+    umma_commit<CG>(bar0 + 8u * (2 * ST + acc));  // tfull[acc]
+}
+
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE>
+__global__ void __launch_bounds__(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1)
+gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p) {
+    using C = Cfg<CG, EW>;
+    using T = typename OutT<OUT>::T;
+    using L = SmemLayout<CG, ST>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    const uint32_t base = (raw_addr + 1023u) & ~1023u;  // SW128 needs 1024-B alignment
+    if (base - raw_addr + L::bytes > L::request) __trap();
+    uint8_t* const smem = smem_raw + (base - raw_addr);
+
+    const uint32_t sA = base + L::a_off;
+    const uint32_t sB = base + L::b_off;
+    const uint32_t bar0 = base + L::bar_off;
+    double2* const tab = reinterpret_cast<double2*>(smem + L::tab_off);
+    ColS* const colbuf = reinterpret_cast<ColS*>(smem + L::col_off);
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (ST + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * ST + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * ST + 2 + a); };
+    const uint32_t tmem_slot = bar0 + 8u * (2 * ST + 4);
+    volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(smem + L::bar_off + 8 * (2 * ST + 4));
+    // pacing words: [0] k-blocks issued by this pair's leader producer, [1] minimum
+    // over all pairs (written by the pacer warp), [2] producer finished
+    volatile uint32_t* s_pace = reinterpret_cast<volatile uint32_t*>(smem + L::pace_off);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = lane_id();
+    const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+    const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+    const int n_clusters = (CG == 2) ? (int)num_clusters_x() : (int)gridDim.x;
+
+    // ---- one-time setup
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&tmap_x);
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), CG * EW);
+        }
+        fence_mbarrier_init();
+        s_pace[0] = 0u;
+        s_pace[1] = 0u;
+        s_pace[2] = 0u;
+    }
+    const int etid = (int)threadIdx.x - kEpiWarp0 * 32;  // epilogue thread id (may be < 0)
+    if (etid >= 0 && etid < 128) tab[etid] = kLog2TabInit[etid];
+    if (warp == 1) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot_ptr;
+
+    const int nkb = p.num_k_blocks;
+    const TileWalk walk{cluster, n_clusters, p.n_full, nkb};
+    // this cluster's split tail unit, if any
+    const int n_tail_units = (p.n_tiles - p.n_full) * p.tail_split;
+    const bool has_tail = p.tail_split > 1 && cluster < n_tail_units;
+    const int tail_t = has_tail ? p.n_full + cluster / p.tail_split : 0;
+    const int tail_c = has_tail ? cluster % p.tail_split : 0;
+    const bool tail_k = has_tail && p.tail_kmode != 0;
+    // N mode: MMA slice width; K mode: full width, K range [kb0, kb1), epilogue slice tail_we
+    const int tail_w = (has_tail && !tail_k) ? C::TS / p.tail_split : C::TS;
+    const int tail_kb0 = tail_k ? (int)((long long)tail_c * nkb / p.tail_split) : 0;
+    const int tail_kb1 = tail_k ? (int)((long long)(tail_c + 1) * nkb / p.tail_split) : nkb;
+    const int tail_we = tail_k ? C::TS / p.tail_epi : tail_w;
+    // L2 pacing: every pair walks K at the same rate over tiles drawn from a few
+    // shared column blocks; kept within a window of one another, the pairs read
+    // the same k-slices of those blocks close together in time, so the L2 serves
+    // them once from HBM instead of once per pair (tall N overflows the L2).
+    // (a separate instantiation: the check costs ~5% in the producer loop of short-K shapes)
+    const bool pacing = PACE && p.pace != nullptr && p.pace_window > 0 && rank == 0 && n_clusters <= kPaceMaxClusters;
+
+    if (warp == 0) {
+        // ================= TMA producer =================
+        if (lane == 0) {
+            const uint64_t policy = p.l2_hint == 1   ? l2_policy_evict_last()
+                                    : p.l2_hint == 2 ? l2_policy_evict_first()
+                                                     : l2_policy_evict_normal();
+            const int pf = p.prefetch_dist;
+            const uint32_t fb_rank = (CG == 2) ? 0u : rank;  // CG == 2: signal the leader's barrier
+            int s = 0;
+            uint32_t ph = 0;
+            for (long long g = 0; g < pf; ++g) {  // warm the L2 with the first pf k-blocks
+                int t, kb;
+                if (!walk.at(g, t, kb)) break;
+                const int2 tile = p.tiles[t];
+                tma_prefetch_3d(&tmap_x, 0, tile.x * C::TS + (int)rank * 128, kb);
+                tma_prefetch_3d(&tmap_x, 0, tile.y * C::TS + (int)rank * 128, kb);
+            }
+            int t, kb;
+            bool pace_on = pacing;
+            const long long win = p.pace_window;
+            for (long long g = 0; walk.at(g, t, kb); ++g) {
+                if (PACE && pace_on && (g & 15) == 0) {
+                    s_pace[0] = (uint32_t)g;
+                    if (g > win) {
+                        // wait (bounded: pacing is only a hint) while the slowest pair is too far behind
+                        int spins = 0;
+                        while ((long long)s_pace[1] + win < g) {
+                            __nanosleep(64);
+                            if (++spins > 20000) { pace_on = false; break; }
+                        }
+                    }
+                }
+                const int2 tile = p.tiles[t];
+                const int rowA = tile.x * C::TS + (int)rank * 128;
+                const int rowB = tile.y * C::TS + (int)rank * 128;
+                int tp, kbp;
+                if (pf > 0 && walk.at(g + pf, tp, kbp)) {
+                    const int2 tpf = p.tiles[tp];
+                    tma_prefetch_3d(&tmap_x, 0, tpf.x * C::TS + (int)rank * 128, kbp);
+                    tma_prefetch_3d(&tmap_x, 0, tpf.y * C::TS + (int)rank * 128, kbp);
+                }
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                const uint32_t fb = (CG == 2) ? map_to_cta(full_bar(s), fb_rank) : full_bar(s);
+                if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
+                tma_load_3d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, 0, rowA, kb, policy);
+                tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
+                if (++s == ST) { s = 0; ph ^= 1u; }
+            }
+            if (has_tail) {
+                const uint2 st = producer_tail<CG, ST>(&tmap_x, p.tiles[tail_t], rank, tail_k ? 0 : tail_c, tail_w,
+                                                       tail_kb0, tail_kb1, sA, sB, bar0, policy, s, ph);
+                s = (int)st.x;
+                ph = st.y;
+            }
+            s_pace[2] = 1u;
+            // drain: the last commit of every stage must land before exit
+            for (int q = 0; q < ST; ++q) {
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                if (++s == ST) { s = 0; ph ^= 1u; }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_i8(C::MMA_M, C::MMA_N);
+            int s = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t aph = 0;
+            int it = 0;
+            for (int t = cluster; t < p.n_full; t += n_clusters, ++it) {
+                mbar_wait(tempty_bar(acc), aph ^ 1u);
+                tc_fence_after();
+                if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 0] = clock64();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(full_bar(s), ph);
+                    tc_fence_after();
+                    const uint64_t adesc = umma_desc_sw128_kmajor(sA + s * kStageHalfBytes);
+                    const uint64_t bdesc = umma_desc_sw128_kmajor(sB + s * kStageHalfBytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 32; ++k) {
+                        // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
+                        umma_i8<CG>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    umma_commit<CG>(empty_bar(s));  // frees the smem slot (both CTAs)
+                    if (++s == ST) { s = 0; ph ^= 1u; }
+                }
+                umma_commit<CG>(tfull_bar(acc));  // accumulator ready (both CTAs)
+                if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 1] = clock64();
+                if (++acc == 2) { acc = 0; aph ^= 1u; }
+            }
+            if (has_tail) mma_tail<CG, ST>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
+        }
+    } else if (PACE && warp == C::PACER_WARP) {
+        // ================= pacer =================
+        if (pacing) {
+            volatile uint32_t* gp = p.pace;
+            if (lane == 0) gp[cluster * kPaceStride] = 0u;
+            uint32_t last = 0u;
+            for (;;) {
+                const uint32_t done = s_pace[2];
+                const uint32_t mine = s_pace[0];
+                if (lane == 0 && mine != last) {
+                    gp[cluster * kPaceStride] = mine;
+                    last = mine;
+                }
+                uint32_t v = 0xFFFFFFFFu;
+                for (int c = (int)lane; c < n_clusters; c += 32) v = min(v, gp[c * kPaceStride]);
+                v = __reduce_min_sync(0xFFFFFFFFu, v);
+                if (lane == 0) s_pace[1] = v;
+                if (done) break;
+                __nanosleep(256);
+            }
+            if (lane == 0) gp[cluster * kPaceStride] = 0xFFFFFFFFu;  // finished pairs never hold others back
+        }
+    } else {
+        // ================= epilogue =================
+        const int q = warp & 3;                          // TMEM lane quadrant of this warp
+        const int part = (warp - kEpiWarp0) >> 2;        // which column slice of the accumulator
+        const int row_local = q * 32 + (int)lane;
+        const int m = p.m;
+        const double dN = (double)p.n_rows;
+        const double rN = 1.0 / dN;
+        named_barrier_sync(1, EW * 32);                  // log2 table is in smem
+        int eNi;
+        const double fN = log2_frac(dN, tab, eNi);       // same routine as the per-column logs
+        const double eN = (double)eNi;
+        const bool have_table = MODE == MI_MODE_EXACT && p.xlogx != nullptr;
+        const long long nln = have_table ? p.xlogx[p.n_rows] : 0ll;  // T(N) = N log2 N 2^s
+        const int64_t ld = p.ld_out;
+        T* __restrict__ out = reinterpret_cast<T*>(p.out);
+        const uint32_t tempty_leader0 = (CG == 2) ? map_to_cta(tempty_bar(0), 0) : tempty_bar(0);
+        const uint32_t tempty_leader1 = (CG == 2) ? map_to_cta(tempty_bar(1), 0) : tempty_bar(1);
+        int acc = 0;
+        uint32_t aph = 0;
+        int it = 0;
+        const bool tracer = p.trace && cluster == 0 && rank == 0 && warp == kEpiWarp0 && lane == 0;
+        // one tile's epilogue, or of one column slice [c0, c0 + W) of a split
+        // tail tile: N mode -- the slice's accumulator in TMEM columns [0, W);
+        // K mode -- this unit's full-width partial plus the other units' ones
+        auto epi_tile = [&](const int t, auto tail_tag) {
+            constexpr int TAIL = decltype(tail_tag)::value;  // 0 whole tile, 1 N slice, 2 K-split owner
+            const int c0 = TAIL ? tail_c * tail_we : 0;       // first tile column of this epilogue
+            const int tc0 = TAIL == 2 ? c0 : 0;                // its accumulator column
+            const int part_cols = TAIL ? tail_we / C::COL_PARTS : C::WARP_COLS;
+            const int2 tile = p.tiles[t];
+            const bool diag = tile.x == tile.y;
+            const int i = tile.x * C::TS + (int)rank * 128 + row_local;
+            ColS* const cols = colbuf + acc * C::TS;   // this tile's column marginals
+            ColS Arow{};
+            RowQ AQ{0, 0, 0};
+            bool use_table = false;
+            if constexpr (OUT != MI_OUT_COUNTS) {
+                if (etid < C::TS) cols[etid] = col_s(p.colstat[tile.y * C::TS + etid]);
+                named_barrier_sync(2, EW * 32);
+                Arow = col_s(p.colstat[i]);  // colstat has m_pad entries
+                AQ = RowQ{Arow.vi, p.n_rows - Arow.vi, nln - Arow.q};
+                // per-tile choice (identical in both CTAs of a pair): table path
+                // when the tile's column sums are clustered enough for the
+                // gathers to hit in L1, FP64 path otherwise
+                if (have_table) {
+                    const int bl = C::TS / 128;
+                    int lo = 0x7FFFFFFF, hi = -1, spread = 0;
+                    for (int q2 = 0; q2 < bl; ++q2) {
+                        const int2 a = p.blkrange[tile.x * bl + q2];
+                        lo = min(lo, a.x);
+                        hi = max(hi, a.y);
+                    }
+                    spread = hi >= lo ? hi - lo : 0;
+                    lo = 0x7FFFFFFF;
+                    hi = -1;
+                    for (int q2 = 0; q2 < bl; ++q2) {
+                        const int2 a = p.blkrange[tile.y * bl + q2];
+                        lo = min(lo, a.x);
+                        hi = max(hi, a.y);
+                    }
+                    spread += hi >= lo ? hi - lo : 0;
+                    use_table = spread <= p.table_thr;
+                }
+            }
+            const RowMarg A = row_marg(Arow, eN, dN);
+            const bool row_ok = i < m;
+            mbar_wait(tfull_bar(acc), aph);
+            tc_fence_after();
+            if (tracer && it < 64) p.trace[it * 4 + 2] = clock64();
+#pragma unroll 1
+            for (int c = 0; c < part_cols; c += 16) {
+                const int col0 = part * part_cols + c;   // accumulator column
+                const int j0 = tile.y * C::TS + c0 + col0;
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
+                tmem_ld_wait(r);
+                if constexpr (TAIL == 2) {  // + the other K ranges (integer adds: exact in any order)
+                    const int u0 = (t - p.n_full) * p.tail_split;
+                    const size_t off = ((size_t)((tc0 + col0) / 16) * 128 + row_local) * 16;
+#pragma unroll 1
+                    for (int w = 0; w < p.tail_split; ++w) {
+                        if (w == tail_c) continue;
+                        const uint4* src = reinterpret_cast<const uint4*>(
+                            p.tail_part + (size_t)((u0 + w) * CG + (int)rank) * 128 * C::TS + off);
+                        uint4 x[4];
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) x[k4] = __ldcg(src + k4);
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {
+                            r[4 * k4 + 0] += x[k4].x;
+                            r[4 * k4 + 1] += x[k4].y;
+                            r[4 * k4 + 2] += x[k4].z;
+                            r[4 * k4 + 3] += x[k4].w;
+                        }
+                    }
+                }
+                const bool vec_ok = ((reinterpret_cast<uintptr_t>(out + (int64_t)i * ld + j0) & (2 * sizeof(T) - 1)) == 0);
+                if (use_table) {
+                    if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
+                        if (diag)
+                            epilogue16<OUT, MODE, true, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab,
+                                                              out, ld, row_ok, vec_ok);
+                        else
+                            epilogue16<OUT, MODE, false, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab,
+                                                               out, ld, row_ok, vec_ok);
+                    }
+                } else if (diag) {
+                    epilogue16<OUT, MODE, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
+                                                       row_ok, vec_ok);
+                } else {
+                    epilogue16<OUT, MODE, false, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
+                                                        row_ok, vec_ok);
+                }
+            }
+            // hand the accumulator back to the MMA warp
+            if (tracer && it < 64) p.trace[it * 4 + 3] = clock64();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            if (p.row_done) {
+                // publish: this CTA's rows and mirrors of tile (I, J) are in memory
+                __threadfence_system();
+                named_barrier_sync(3, EW * 32);
+                if (etid == 0) atomicAdd_system(p.row_done + tile.x, 1u);
+            }
+            if (++acc == 2) { acc = 0; aph ^= 1u; }
+        };
+        // per-cluster timeline (globaltimer ns): start, main tiles done, tail done
+        long long* const ctrace = (p.trace && rank == 0 && etid == 0) ? p.trace + 256 + cluster * 4 : nullptr;
+        if (ctrace) ctrace[0] = (long long)global_ns();
+        for (int t = cluster; t < p.n_full; t += n_clusters, ++it) epi_tile(t, std::integral_constant<int, 0>{});
+        if (ctrace) ctrace[1] = (long long)global_ns();
+        if (has_tail && !tail_k) {
+            epi_tile(tail_t, std::integral_constant<int, 1>{});
+        } else if (has_tail) {
+            // K-split unit: publish the partial accumulator (all columns) ...
+            mbar_wait(tfull_bar(acc), aph);
+            tc_fence_after();
+            uint32_t* dst_base = p.tail_part + (size_t)(cluster * CG + (int)rank) * 128 * C::TS;
+#pragma unroll 1
+            for (int c = 0; c < C::WARP_COLS; c += 16) {
+                const int col0 = part * C::WARP_COLS + c;
+                uint32_t r[16];
+                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + col0), r);
+                tmem_ld_wait(r);
+                uint4* dst = reinterpret_cast<uint4*>(dst_base + ((size_t)(col0 / 16) * 128 + row_local) * 16);
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4)
+                    __stcg(dst + k4, make_uint4(r[4 * k4], r[4 * k4 + 1], r[4 * k4 + 2], r[4 * k4 + 3]));
+            }
+            __threadfence();
+            named_barrier_sync(4, EW * 32);
+            unsigned int* flag = p.tail_flag + (tail_t - p.n_full) * 2 + rank;
+            if (etid == 0) atomicAdd(flag, 1u);
+            if (tail_c < p.tail_epi) {
+                // ... then, as an epilogue unit, wait for every unit's partial and
+                // finish column slice tail_c on the sum
+                if (etid == 0) {
+                    volatile unsigned int* f = flag;
+                    const long long t0 = clock64();
+                    while (*f < (unsigned int)p.tail_split) {
+                        __nanosleep(64);
+                        if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: a lost unit is a bug
+                    }
+                    __threadfence();
+                }
+                named_barrier_sync(4, EW * 32);
+                epi_tile(tail_t, std::integral_constant<int, 2>{});
+            } else {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            }
+        }
+        if (ctrace) ctrace[2] = (long long)global_ns();
+    }
+
+    // ---- teardown
+    __syncwarp();
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+}
+
+// ---------------------------------------------------------------- launch
+
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE>
+cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream) {
+    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW, PACE>;
+    constexpr uint32_t smem = SmemLayout<CG, ST>::request;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int max_clusters = num_sms / CG;
+    int clusters = p.n_tiles < max_clusters ? p.n_tiles : max_clusters;
+    if (p.tail_split > 1) {  // the host sized n_full as a multiple of max_clusters
+        if (p.n_full % max_clusters != 0 || (p.n_tiles - p.n_full) * p.tail_split > max_clusters)
+            return cudaErrorInvalidValue;
+        clusters = p.n_full > 0 ? max_clusters : (p.n_tiles - p.n_full) * p.tail_split;
+    }
+    if (clusters < 1) clusters = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CG, 1, 1);
+    cfg.blockDim = dim3(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmap, p);
+}
+
+}  // namespace mib200

@@ -40,9 +40,27 @@ struct GramMiParams {
                             // stored (system scope; lets the host stream finished rows to host)
     unsigned int* pace;     // optional: per-cluster k-block progress, stride kPaceStride (L2 pacing)
     int pace_window;        // leader producers stay within this many k-blocks of the slowest pair (0 = off)
+    // Tail split of the last, partial round: tiles [0, n_full) are dealt
+    // whole, round robin; each of the n_tiles - n_full tail tiles becomes
+    // tail_split units run by clusters u = (t - n_full) * tail_split + c:
+    //  tail_kmode 0 (short K): unit c = column slice [c W, (c + 1) W) of the
+    //    tile with the full K range, W = TS / tail_split -- no partial sums;
+    //  tail_kmode 1 (long K; a narrow slice would be load-bound): unit c = K
+    //    range c of the full tile.  Every unit stores its int32 accumulator in
+    //    tail_part (slot u, 128 x TS per CTA) and bumps tail_flag[(t - n_full)
+    //    * 2 + rank] (zeroed by the host before the launch); units c <
+    //    tail_epi then wait for all tail_split partials and run the epilogue
+    //    of column slice c (TS / tail_epi wide) on their sum.
+    int n_full;
+    int tail_split;         // 1 = no split
+    int tail_kmode;
+    int tail_epi;
+    unsigned int* tail_flag;
+    uint32_t* tail_part;
 };
 constexpr int kPaceStride = 8;          // u32 per cluster slot (one 32-B sector each)
 constexpr int kPaceMaxClusters = 256;
+constexpr int kTailMaxUnits = 148;      // split tail units (<= clusters): flag pairs and partial slots
 constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
 
 cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,

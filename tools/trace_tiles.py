@@ -14,13 +14,24 @@ w = datagen.generate_words_device(rec, eng.device)
 prep = eng.prepare(w, n, m)
 out = torch.empty((m, m), dtype=dt, device=eng.device)
 eng.compute(prep, None, dt, out=out)
-tr = torch.zeros(64 * 4, dtype=torch.int64, device=eng.device)
+tr = torch.zeros(64 * 4 + 256 * 4, dtype=torch.int64, device=eng.device)
 nat.lib().mi_debug_set_trace.argtypes = [ctypes.c_void_p]
 nat.lib().mi_debug_set_trace(tr.data_ptr())
 eng.compute(prep, None, dt, out=out)
 torch.cuda.synchronize()
 nat.lib().mi_debug_set_trace(None)
-t = tr.view(64, 4).cpu().tolist()
+allt = tr.cpu()
+t = allt[:256].view(64, 4).tolist()
+ct = allt[256:].view(256, 4)
+ct = ct[ct[:, 0] != 0]
+if len(ct):
+    base = int(ct[:, 0].min())
+    st, md, en = (ct[:, 0] - base) / 1e3, (ct[:, 1] - base) / 1e3, (ct[:, 2] - base) / 1e3
+    print(f"clusters {len(ct)}: start spread {float(st.max()):.1f} us; main-done min/med/max "
+          f"{float(md.min()):.1f}/{float(md.median()):.1f}/{float(md.max()):.1f} us; "
+          f"end min/med/max {float(en.min()):.1f}/{float(en.median()):.1f}/{float(en.max()):.1f} us")
+    order = torch.argsort(en, descending=True)[:8].tolist()
+    print("  slowest clusters (id: main_done, end):", ", ".join(f"{i}: {float(md[i]):.0f}, {float(en[i]):.0f}" for i in order))
 t0 = t[0][0]
 print(f"cfg{cfg} {dt}: cycles relative to first MMA start (k = 1000 cycles)")
 print(" tile  mma_start mma_end(issue)  epi_start  epi_end   mma_len epi_len  mma_wait_for_acc")
