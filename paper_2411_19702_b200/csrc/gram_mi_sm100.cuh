@@ -184,6 +184,27 @@ __device__ __forceinline__ void store_pair(int32_t* p, int32_t a, int32_t b) {
     *reinterpret_cast<int2*>(p) = make_int2(a, b);
 }
 
+// One 32-byte store (STG.256, sm_100): a full L2 sector per thread.  The
+// direct-tile stores are the epilogue's only stores that are not coalesced
+// across the warp (32 rows per instruction); at 16 bytes per thread they cost
+// ~6% of the MMA rate at config 3 (half-sector writes), measured with the
+// debug store masks.
+__device__ __forceinline__ void store32(double* p, const double* v) {
+    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(__double_as_longlong(v[0])),
+                 "l"(__double_as_longlong(v[1])), "l"(__double_as_longlong(v[2])), "l"(__double_as_longlong(v[3]))
+                 : "memory");
+}
+__device__ __forceinline__ void store32(float* p, const float* v) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void store32(int32_t* p, const int32_t* v) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 // The tile row's fixed-point marginals (table path).
 struct RowQ {
     int v, nmv;      // v_i, N - v_i
@@ -241,7 +262,7 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
             v[k] = (T)x;
         }
     }
-    if (p.debug) {  // keep the math alive without storing the tile
+    if (p.debug & 1) {  // keep the math alive without storing the tile
         T acc = v[0];
 #pragma unroll
         for (int k = 1; k < 16; ++k) acc = acc + v[k];
@@ -250,13 +271,19 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
     }
     if (!row_ok) return;
     // 2) mirror tile: row j, column i (coalesced across the warp)
-    if (!DIAG) {
+    if (!DIAG && !(p.debug & 2)) {
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             if (j0 + k < m) out[(int64_t)(j0 + k) * ld + i] = v[k];
     }
     // 3) direct tile: row i, columns j0 .. j0+15
+    if (p.debug & 4) return;
     T* dst = out + (int64_t)i * ld + j0;
+    if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0 && j0 + 15 < m) {
+#pragma unroll
+        for (int k = 0; k < 16; k += 32 / (int)sizeof(T)) store32(dst + k, v + k);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 16; k += 2) {
         if (vec_ok && j0 + k + 1 < m) {
