@@ -10,9 +10,9 @@
 // The same pass produces v[c] = popcount of column c, i.e. the reference's
 // column_sums (binmat.py:175-177), which the fused epilogue needs.
 //
-// HBM-bound: reads 8*m*nw bytes, writes m_pad*N_pad bytes.  One warp per
-// column; each lane expands 16 bits into one 16-byte store so a warp
-// instruction writes 512 contiguous bytes.
+// HBM-bound: reads 8*m*nw bytes, writes m_pad*N_pad bytes.  Blocks of 32
+// columns transpose through shared memory so that both the word reads and the
+// byte writes are long contiguous runs (below).
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -25,12 +25,18 @@ namespace mib200 {
 // so the multiply places bit k at bit 8k with no carries).
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
-// T(c) = c log2(c) 2^s for c = 0..N with the epilogue's own fix_xlog2x, so the
+// Prologue: zero the per-column count accumulators (ColStat::vi), reset the
+// per-128-column (min, max) column sums, and build T(c) = c log2(c) 2^s for
+// c = 0..N (when xlogx != nullptr) with the epilogue's own fix_xlog2x, so the
 // table path and the per-column terms agree bit for bit.
-__global__ void __launch_bounds__(256) xlogx_table_kernel(long long* __restrict__ T, long long N, int s,
+__global__ void __launch_bounds__(256) unpack_prep_kernel(ColStat* __restrict__ colstat, int64_t m_pad,
+                                                          long long* __restrict__ T, long long N, int s,
                                                           int2* __restrict__ blkrange, int nblk) {
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
-        blkrange[b] = make_int2(0x7FFFFFFF, -1);  // (min, max) column sum, filled by the unpack
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = tid; c < m_pad; c += nthr) colstat[c].vi = 0;
+    for (int64_t b = tid; b < nblk; b += nthr) blkrange[b] = make_int2(0x7FFFFFFF, -1);
+    if (!T) return;
     __shared__ float R[1 << kFixLogBits];
     __shared__ float2 LG[1 << kFixLogBits];
     for (int q = threadIdx.x; q < (1 << kFixLogBits); q += blockDim.x) {
@@ -38,82 +44,152 @@ __global__ void __launch_bounds__(256) xlogx_table_kernel(long long* __restrict_
         LG[q] = kFixLG[q];
     }
     __syncthreads();
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c <= N; c += (long long)gridDim.x * blockDim.x)
-        T[c] = fix_xlog2x((unsigned)c, s, R, LG);
+    for (long long c = tid; c <= N; c += nthr) T[c] = fix_xlog2x((unsigned)c, s, R, LG);
+}
+
+// Per-column statistics for the fused epilogue (lane/thread owning column c).
+__device__ __forceinline__ void write_colstat(int64_t c, uint32_t cnt, int64_t n_rows, bool real, int fix_s,
+                                              int32_t* __restrict__ colsum, ColStat* __restrict__ colstat,
+                                              int2* __restrict__ blkrange) {
+    if (colsum) colsum[c] = (int32_t)cnt;
+    // marginal logs for the fused epilogue: log2(v) and log2(N - v)
+    ColStat st;
+    const int64_t v0 = n_rows - (int64_t)cnt;
+    int e1 = 0, e0 = 0;
+    st.v = (double)cnt;
+    st.nv = (double)v0;
+    st.f1 = cnt > 0 ? log2_frac((double)cnt, kLog2TabInit, e1) : 0.0;
+    st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, e0) : 0.0;
+    st.e1 = cnt > 0 ? (double)e1 : 0.0;
+    st.e0 = v0 > 0 ? (double)e0 : 0.0;
+    st.vi = (int)cnt;
+    st.pad = 0;
+    st.q = fix_xlog2x(cnt, fix_s, kFixR, kFixLG) + fix_xlog2x((unsigned)v0, fix_s, kFixR, kFixLG);
+    if (blkrange && real) {
+        atomicMin(&blkrange[c / 128].x, (int)cnt);
+        atomicMax(&blkrange[c / 128].y, (int)cnt);
+    }
+    colstat[c] = st;
+}
+
+// Expansion: block (g, k) owns 32 columns c0 = 32 g .. c0 + 31 and K chunk k
+// (kUnpackTiles tiles of 64 words).  Each tile's 32 x 512 bytes of words are
+// staged in shared memory by cp.async (double-buffered: tile i + 1 loads while
+// tile i expands); then every warp expands whole k-blocks: lane l owns column
+// c0 + l, turns its 2 words into 128 bytes (four STG.256), and the warp's
+// stores fill one contiguous 4 KB run of X (the group's 32 rows of one
+// k-block).  Ones are counted on the fly into ColStat::vi.
+constexpr int kUnpackCols = 32;
+constexpr int kUnpackWords = 64;                // words per column per K tile (= 32 k-blocks)
+constexpr int kUnpackPitch = kUnpackWords + 1;  // smem row pitch in words (2-way banks at most)
+constexpr int kUnpackTiles = 4;                 // tiles per block (K chunk = 256 words)
+
+__device__ __forceinline__ void store_row128(int8_t* dst, uint64_t w0, uint64_t w1) {
+    uint32_t q[32];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        q[k] = spread4((uint32_t)(w0 >> (4 * k)) & 0xFu);
+        q[16 + k] = spread4((uint32_t)(w1 >> (4 * k)) & 0xFu);
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 32 * h),
+                     "r"(q[8 * h + 0]), "r"(q[8 * h + 1]), "r"(q[8 * h + 2]), "r"(q[8 * h + 3]), "r"(q[8 * h + 4]),
+                     "r"(q[8 * h + 5]), "r"(q[8 * h + 6]), "r"(q[8 * h + 7])
+                     : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* src, bool valid) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
 
 __global__ void __launch_bounds__(256)
-unpack_colsum_kernel(const uint64_t* __restrict__ words, int64_t n_rows, int64_t m, int64_t nw,
-                     int8_t* __restrict__ x, int64_t ld, int64_t m_pad, int32_t* __restrict__ colsum,
-                     ColStat* __restrict__ colstat, int fix_s, int2* __restrict__ blkrange) {
-    const int lane = threadIdx.x & 31;
-    const int quarter = lane & 3;
-    const int64_t warp0 = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x / 32);
-    const int64_t wpad = ld / 64;  // words per padded column
-    for (int64_t c = warp0; c < m_pad; c += nwarps) {
-        const uint64_t* __restrict__ src = words + c * nw;
-        int8_t* __restrict__ dst = x + c * 128;  // row c inside every k-block
-        const int64_t kb_stride = m_pad * 128;
-        const bool real = c < m;
-        uint32_t cnt = 0;
-#pragma unroll 4
-        for (int64_t base = 0; base < wpad; base += 8) {
-            const int64_t w = base + (lane >> 2);
-            const uint64_t word = (real && w < nw) ? __ldg(src + w) : 0ull;
-            const uint32_t b16 = (uint32_t)(word >> (16 * quarter)) & 0xFFFFu;
-            cnt += __popc(b16);
-            uint4 v;
-            v.x = spread4(b16 & 0xF);
-            v.y = spread4((b16 >> 4) & 0xF);
-            v.z = spread4((b16 >> 8) & 0xF);
-            v.w = spread4(b16 >> 12);
-            if (w < wpad)
-                *reinterpret_cast<uint4*>(dst + (w >> 1) * kb_stride + (w & 1) * 64 + quarter * 16) = v;
-        }
+unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x, int64_t ld,
+              int64_t m_pad, ColStat* __restrict__ colstat) {
+    __shared__ __align__(16) uint64_t tile[2][kUnpackCols * kUnpackPitch];
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const int64_t wpad = ld / 64;  // words per padded column (even)
+    const int64_t nkb = ld / 128;
+    const int64_t kb_stride = m_pad * 128;
+    const int ld_col = t >> 3;     // loader: column of the group
+    const int ld_sub = t & 7;      // loader: 8 words of the tile row
+    const int64_t c0 = (int64_t)blockIdx.x * kUnpackCols;
+    const int64_t lc = c0 + ld_col;
+    const bool lreal = lc < m;
+    const uint64_t* __restrict__ src = words + (lreal ? lc : 0) * nw;
+    const int64_t wbeg = (int64_t)blockIdx.y * kUnpackTiles * kUnpackWords;
+    int ntiles = (int)((wpad - wbeg + kUnpackWords - 1) / kUnpackWords);
+    if (ntiles > kUnpackTiles) ntiles = kUnpackTiles;
+    auto issue = [&](int i) {
+        uint64_t* dstrow = &tile[i & 1][ld_col * kUnpackPitch + ld_sub * 8];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) {
-            if (colsum) colsum[c] = (int32_t)cnt;
-            // marginal logs for the fused epilogue: log2(v) and log2(N - v)
-            ColStat st;
-            const int64_t v0 = n_rows - (int64_t)cnt;
-            int e1 = 0, e0 = 0;
-            st.v = (double)cnt;
-            st.nv = (double)v0;
-            st.f1 = cnt > 0 ? log2_frac((double)cnt, kLog2TabInit, e1) : 0.0;
-            st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, e0) : 0.0;
-            st.e1 = cnt > 0 ? (double)e1 : 0.0;
-            st.e0 = v0 > 0 ? (double)e0 : 0.0;
-            st.vi = (int)cnt;
-            st.pad = 0;
-            st.q = fix_xlog2x(cnt, fix_s, kFixR, kFixLG) + fix_xlog2x((unsigned)v0, fix_s, kFixR, kFixLG);
-            if (blkrange && real) {
-                atomicMin(&blkrange[c / 128].x, (int)cnt);
-                atomicMax(&blkrange[c / 128].y, (int)cnt);
-            }
-            colstat[c] = st;
+        for (int k = 0; k < 8; ++k) {
+            const int64_t w = wbeg + (int64_t)i * kUnpackWords + ld_sub * 8 + k;
+            const bool ok = lreal && w < nw;
+            cp_async8(dstrow + k, src + (ok ? w : 0), ok);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    uint32_t cnt = 0;
+    issue(0);
+    for (int i = 0; i < ntiles; ++i) {
+        if (i + 1 < ntiles) {
+            issue(i + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const uint64_t* buf = tile[i & 1];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cnt += __popcll(buf[ld_col * kUnpackPitch + ld_sub * 8 + k]);
+        const int64_t kb0 = (wbeg + (int64_t)i * kUnpackWords) / 2;
+#pragma unroll
+        for (int kk = 0; kk < kUnpackWords / 2; kk += 8) {
+            const int kbl = kk + warp;
+            if (kb0 + kbl < nkb)
+                store_row128(x + (kb0 + kbl) * kb_stride + (c0 + lane) * 128, buf[lane * kUnpackPitch + 2 * kbl],
+                             buf[lane * kUnpackPitch + 2 * kbl + 1]);
+        }
+        __syncthreads();  // buffer i & 1 is reloaded by issue(i + 2)
     }
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
+    if (ld_sub == 0 && cnt) atomicAdd(&colstat[lc].vi, (int)cnt);
+}
+
+// Epilogue of kernel 1: per-column statistics from the finished counts.
+__global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m, int64_t m_pad,
+                                                      int32_t* __restrict__ colsum, ColStat* __restrict__ colstat,
+                                                      int fix_s, int2* __restrict__ blkrange) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m_pad; c += (int64_t)gridDim.x * blockDim.x)
+        write_colstat(c, (uint32_t)colstat[c].vi, n_rows, c < m, fix_s, colsum, colstat, blkrange);
 }
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
                                  int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, long long* xlogx,
                                  int2* blkrange, int num_sms, cudaStream_t stream) {
-    if (xlogx) {
-        int64_t tb = (n_rows + 1 + 255) / 256;
+    const int fix_s = xlogx_scale(n_rows);
+    {
+        int64_t work = xlogx ? n_rows + 1 : 0;
+        if (work < m_pad) work = m_pad;
+        int64_t tb = (work + 255) / 256;
         if (tb > (int64_t)num_sms * 16) tb = (int64_t)num_sms * 16;
-        xlogx_table_kernel<<<(unsigned)tb, 256, 0, stream>>>(xlogx, n_rows, xlogx_scale(n_rows), blkrange,
-                                                              blkrange ? (int)(m_pad / 128) : 0);
+        unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, xlogx, n_rows, fix_s, blkrange,
+                                                             (xlogx && blkrange) ? (int)(m_pad / 128) : 0);
     }
-    const int threads = 256;
-    int64_t blocks = (m_pad + 7) / 8;
-    const int64_t cap = (int64_t)num_sms * 8;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    unpack_colsum_kernel<<<(unsigned)blocks, threads, 0, stream>>>(words, n_rows, m, nw, x, ld, m_pad, colsum,
-                                                                   colstat, xlogx_scale(n_rows),
-                                                                   xlogx ? blkrange : nullptr);
+    const int64_t wpad = ld / 64;
+    const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);
+    if (chunks > 65535) return cudaErrorInvalidValue;
+    unpack_kernel<<<dim3((unsigned)(m_pad / kUnpackCols), (unsigned)chunks), 256, 0, stream>>>(words, m, nw, x, ld,
+                                                                                              m_pad, colstat);
+    int64_t cb = (m_pad + 255) / 256;
+    if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
+    colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, m_pad, colsum, colstat, fix_s,
+                                                     xlogx ? blkrange : nullptr);
     return cudaGetLastError();
 }
 
