@@ -56,17 +56,22 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
                        env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8),
                        env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
-                       env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1)};
+                       env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
+// Operand format: e2m1 nibbles for kind::mxf4 (twice the int8 MMA rate, half
+// the bytes) on SM pairs while fp32 accumulation is exact (N < 2^24), else
+// int8.  mi_unpack_colsum and mi_gram_mi both follow this rule, so the knob
+// must not change between them.
+bool operand_fp4(int64_t n_rows) { return tuning().fp4 && tuning().cta_group == 2 && n_rows < kFp4MaxN; }
 int prefetch_dist() { return tuning().prefetch; }
 int l2_hint() { return tuning().l2_hint; }
 int tile_band() { return tuning().band > 0 ? tuning().band : 8; }
@@ -372,7 +377,8 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
     MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
                                  (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
-                                 blkrange_ptr(ws.colstat, n_rows, n_cols), info.num_sms, ws.stream));
+                                 blkrange_ptr(ws.colstat, n_rows, n_cols), operand_fp4(n_rows), info.num_sms,
+                                 ws.stream));
     *ld_out = ld;
     *m_pad_out = m_pad;
     return MI_OK;
@@ -424,7 +430,10 @@ int mi_device_info(int device, int* num_sms, int* cc_major, int* cc_minor) {
     return rc;
 }
 
-int64_t mi_kmajor_ld(int64_t n_rows) { return round_up(n_rows < 1 ? 1 : n_rows, 128); }
+int64_t mi_kmajor_ld(int64_t n_rows) {
+    const int64_t n = n_rows < 1 ? 1 : n_rows;
+    return operand_fp4(n) ? round_up(n, 256) / 2 : round_up(n, 128);
+}
 
 int64_t mi_kmajor_rows(int64_t n_cols) { return round_up(n_cols < 1 ? 1 : n_cols, 256); }
 
@@ -474,7 +483,8 @@ int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, in
     if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
     MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
                                  (ColStat*)d_colstat, xlogx_ptr(d_colstat, n_rows, n_cols),
-                                 blkrange_ptr(d_colstat, n_rows, n_cols), info.num_sms, (cudaStream_t)stream));
+                                 blkrange_ptr(d_colstat, n_rows, n_cols), operand_fp4(n_rows), info.num_sms,
+                                 (cudaStream_t)stream));
     return MI_OK;
 }
 
@@ -547,7 +557,8 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.table_thr = tuning().fixed == 0 ? -1 : tuning().fixed == 2 ? 0x7FFFFFFF : tuning().table_thr;
     int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
-    MI_CUDA(launch_gram_mi(cta_group(), out_kind, eff_mode, tuning().stages, tuning().epi_warps, tm, p, info.num_sms, stream));
+    MI_CUDA(launch_gram_mi(cta_group(), operand_fp4(n_rows), out_kind, eff_mode, tuning().stages, tuning().epi_warps,
+                           tm, p, info.num_sms, stream));
     return MI_OK;
 }
 
@@ -718,6 +729,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "tail")) {
         if (value < 0 || value > 3) return fail(MI_ERR_DOMAIN, "tail must be 0 (off), 1 (auto), 2 (slices) or 3 (K ranges)");
         t.tail = value;
+    } else if (!strcmp(key, "fp4")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "fp4 must be 0 (int8 operands) or 1");
+        t.fp4 = value;
     } else if (!strcmp(key, "pace")) {
         if (value < -1) return fail(MI_ERR_DOMAIN, "pace must be -1 (auto), 0 (off) or a window in k-blocks");
         t.pace = value;
@@ -743,6 +757,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "table_thr")) return t.table_thr;
     if (!strcmp(key, "pace")) return t.pace;
     if (!strcmp(key, "tail")) return t.tail;
+    if (!strcmp(key, "fp4")) return t.fp4;
     return -1;
 }
 

@@ -2,9 +2,9 @@
 #include "gram_mi_sm100.cuh"
 
 namespace mib200 {
-template cudaError_t launch_impl<1, MI_OUT_F64, MI_MODE_EXACT, 6, 8, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
-template cudaError_t launch_impl<1, MI_OUT_F64, MI_MODE_EPSILON, 6, 8, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
-template cudaError_t launch_impl<1, MI_OUT_F32, MI_MODE_EXACT, 6, 8, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
-template cudaError_t launch_impl<1, MI_OUT_F32, MI_MODE_EPSILON, 6, 8, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
-template cudaError_t launch_impl<1, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+template cudaError_t launch_impl<1, MI_OUT_F64, MI_MODE_EXACT, 6, 8, false, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+template cudaError_t launch_impl<1, MI_OUT_F64, MI_MODE_EPSILON, 6, 8, false, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+template cudaError_t launch_impl<1, MI_OUT_F32, MI_MODE_EXACT, 6, 8, false, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+template cudaError_t launch_impl<1, MI_OUT_F32, MI_MODE_EPSILON, 6, 8, false, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+template cudaError_t launch_impl<1, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8, false, false>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
 }  // namespace mib200

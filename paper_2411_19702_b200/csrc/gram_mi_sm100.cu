@@ -4,8 +4,9 @@
 
 namespace mib200 {
 
-#define MI_EXTERN(CGV, OV, MV, PV) \
-    extern template cudaError_t launch_impl<CGV, OV, MV, 6, 8, PV>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+#define MI_EXTERN4(CGV, OV, MV, PV, FV) \
+    extern template cudaError_t launch_impl<CGV, OV, MV, 6, 8, PV, FV>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+#define MI_EXTERN(CGV, OV, MV, PV) MI_EXTERN4(CGV, OV, MV, PV, false)
 MI_EXTERN(2, MI_OUT_F64, MI_MODE_EXACT, false)
 MI_EXTERN(2, MI_OUT_F64, MI_MODE_EPSILON, false)
 MI_EXTERN(2, MI_OUT_F32, MI_MODE_EXACT, false)
@@ -21,20 +22,33 @@ MI_EXTERN(1, MI_OUT_F64, MI_MODE_EPSILON, false)
 MI_EXTERN(1, MI_OUT_F32, MI_MODE_EXACT, false)
 MI_EXTERN(1, MI_OUT_F32, MI_MODE_EPSILON, false)
 MI_EXTERN(1, MI_OUT_COUNTS, MI_MODE_EXACT, false)
+MI_EXTERN4(2, MI_OUT_F64, MI_MODE_EXACT, false, true)
+MI_EXTERN4(2, MI_OUT_F64, MI_MODE_EPSILON, false, true)
+MI_EXTERN4(2, MI_OUT_F32, MI_MODE_EXACT, false, true)
+MI_EXTERN4(2, MI_OUT_F32, MI_MODE_EPSILON, false, true)
+MI_EXTERN4(2, MI_OUT_COUNTS, MI_MODE_EXACT, false, true)
+MI_EXTERN4(2, MI_OUT_F64, MI_MODE_EXACT, true, true)
+MI_EXTERN4(2, MI_OUT_F64, MI_MODE_EPSILON, true, true)
+MI_EXTERN4(2, MI_OUT_F32, MI_MODE_EXACT, true, true)
+MI_EXTERN4(2, MI_OUT_F32, MI_MODE_EPSILON, true, true)
+MI_EXTERN4(2, MI_OUT_COUNTS, MI_MODE_EXACT, true, true)
 #undef MI_EXTERN
+#undef MI_EXTERN4
 
-cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,
-                           const GramMiParams& p, int num_sms, cudaStream_t stream) {
+cudaError_t launch_gram_mi(int cg, bool fp4, int out_kind, int mode, int stages, int epi_warps,
+                           const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream) {
     const bool pace = p.pace != nullptr && p.pace_window > 0;
-#define MI_DISPATCH_P(CGV, OV, MV, STV, EWV, PV)                                                               \
-    if (cg == CGV && out_kind == OV && mode == MV && stages == STV && epi_warps == EWV && pace == PV) \
-        return launch_impl<CGV, OV, MV, STV, EWV, PV>(tmap, p, num_sms, stream);
-#define MI_DISPATCH(CGV, OV, MV, STV, EWV) MI_DISPATCH_P(CGV, OV, MV, STV, EWV, false)
-    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EXACT, 6, 8)
-    MI_DISPATCH(2, MI_OUT_F64, MI_MODE_EPSILON, 6, 8)
-    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8)
-    MI_DISPATCH(2, MI_OUT_F32, MI_MODE_EPSILON, 6, 8)
-    MI_DISPATCH(2, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
+#define MI_DISPATCH_PF(CGV, OV, MV, STV, EWV, PV, FV)                                                            \
+    if (cg == CGV && out_kind == OV && mode == MV && stages == STV && epi_warps == EWV && pace == PV && fp4 == FV) \
+        return launch_impl<CGV, OV, MV, STV, EWV, PV, FV>(tmap, p, num_sms, stream);
+#define MI_DISPATCH_P(CGV, OV, MV, STV, EWV, PV) \
+    MI_DISPATCH_PF(CGV, OV, MV, STV, EWV, PV, false) MI_DISPATCH_PF(CGV, OV, MV, STV, EWV, PV, true)
+#define MI_DISPATCH(CGV, OV, MV, STV, EWV) MI_DISPATCH_PF(CGV, OV, MV, STV, EWV, false, false)
+    MI_DISPATCH_P(2, MI_OUT_F64, MI_MODE_EXACT, 6, 8, false)
+    MI_DISPATCH_P(2, MI_OUT_F64, MI_MODE_EPSILON, 6, 8, false)
+    MI_DISPATCH_P(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8, false)
+    MI_DISPATCH_P(2, MI_OUT_F32, MI_MODE_EPSILON, 6, 8, false)
+    MI_DISPATCH_P(2, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8, false)
     MI_DISPATCH_P(2, MI_OUT_F64, MI_MODE_EXACT, 6, 8, true)
     MI_DISPATCH_P(2, MI_OUT_F64, MI_MODE_EPSILON, 6, 8, true)
     MI_DISPATCH_P(2, MI_OUT_F32, MI_MODE_EXACT, 6, 8, true)
@@ -47,12 +61,14 @@ cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_w
     MI_DISPATCH(1, MI_OUT_COUNTS, MI_MODE_EXACT, 6, 8)
 #undef MI_DISPATCH
 #undef MI_DISPATCH_P
+#undef MI_DISPATCH_PF
+    if (fp4 && cg != 2) return cudaErrorInvalidValue;  // e2m1 operands: SM-pair builds only
     // knob combinations without a dedicated build fall back to the default build of the variant
-    if (stages != 6 || epi_warps != 8) return launch_gram_mi(cg, out_kind, mode, 6, 8, tmap, p, num_sms, stream);
+    if (stages != 6 || epi_warps != 8) return launch_gram_mi(cg, fp4, out_kind, mode, 6, 8, tmap, p, num_sms, stream);
     if (pace) {  // no paced build of this variant (CG == 1)
         GramMiParams q = p;
         q.pace = nullptr;
-        return launch_gram_mi(cg, out_kind, mode, stages, epi_warps, tmap, q, num_sms, stream);
+        return launch_gram_mi(cg, fp4, out_kind, mode, stages, epi_warps, tmap, q, num_sms, stream);
     }
     return cudaErrorInvalidValue;
 }

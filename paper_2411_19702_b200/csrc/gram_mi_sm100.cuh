@@ -310,6 +310,31 @@ struct TileWalk {
 
 // The split tail unit's producer and MMA loops live out of line: inlined after
 // the main loops they cost ~3% of the main loops' throughput (code layout).
+// Operand format: FP4 = e2m1 nibbles (1.0 = 0b0010) through kind::mxf4 with
+// all block scales 1.0 (E8M0 127, TMEM columns [256, 512)), fp32 accumulators
+// (exact integer counts below 2^24 rows), K = 256 per 128-byte k-block, at
+// twice the kind::i8 rate (tools/micro/mxf4_probe.cu).  The scale factors take
+// TMEM beyond one 256-column accumulator, so FP4 runs single-buffered.
+constexpr uint32_t kSfCol = 256;
+template <int CG, bool FP4>
+__device__ __forceinline__ void mma_step(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t tmem_base, uint32_t acc) {
+    if constexpr (FP4) umma_mxf4<CG>(d_tmem, adesc, bdesc, idesc, tmem_base + kSfCol, tmem_base + kSfCol, acc);
+    else umma_i8<CG>(d_tmem, adesc, bdesc, idesc, acc);
+}
+template <int CG, bool FP4>
+__host__ __device__ constexpr uint32_t mma_idesc(int M, int N) {
+    return FP4 ? umma_idesc_mxf4(M, N) : umma_idesc_i8(M, N);
+}
+// accumulator words -> integer counts
+template <bool FP4>
+__device__ __forceinline__ void acc_to_counts(uint32_t (&r)[16]) {
+    if constexpr (FP4) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) r[k] = __float2uint_rz(__uint_as_float(r[k]));
+    }
+}
+
 // Tail units (GramMiParams::tail_*): column slice c (rows of B from
 // J TS + c W + rank W / CG; the TMA box still moves 128 rows, the MMA reads the
 // first W / CG) over k-blocks [kb0, kb1), the full K range for slices.
@@ -332,11 +357,11 @@ __device__ __noinline__ uint2 producer_tail(const CUtensorMap* tmap, int2 tile, 
     return make_uint2((uint32_t)s, ph);
 }
 
-template <int CG, int ST>
+template <int CG, int ST, bool FP4>
 __device__ __noinline__ void mma_tail(uint32_t tmem_base, int width, int kb0, int kb1, uint32_t sA, uint32_t sB,
                                       uint32_t bar0, int s, uint32_t ph, int acc, uint32_t aph) {
     using C = Cfg<CG, 8>;
-    const uint32_t idesc = umma_idesc_i8(C::MMA_M, width);  // M x W accumulator in TMEM columns [0, W)
+    const uint32_t idesc = mma_idesc<CG, FP4>(C::MMA_M, width);  // M x W accumulator in TMEM columns [0, W)
     mbar_wait(bar0 + 8u * (2 * ST + 2 + acc), aph ^ 1u);  // tempty[acc]
     tc_fence_after();
     const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
@@ -347,14 +372,14 @@ __device__ __noinline__ void mma_tail(uint32_t tmem_base, int width, int kb0, in
         const uint64_t bdesc = umma_desc_sw128_kmajor(sB + s * kStageHalfBytes);
 #pragma unroll
         for (int k = 0; k < kBK / 32; ++k)
-            umma_i8<CG>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            mma_step<CG, FP4>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, tmem_base, (kb != kb0 || k != 0) ? 1u : 0u);
         umma_commit<CG>(bar0 + 8u * (ST + s));  // empty[s]
         if (++s == ST) { s = 0; ph ^= 1u; }
     }
     umma_commit<CG>(bar0 + 8u * (2 * ST + acc));  // tfull[acc]
 }
 
-template <int CG, int OUT, int MODE, int ST, int EW, bool PACE>
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE, bool FP4>
 __global__ void __launch_bounds__(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1)
 gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p) {
     using C = Cfg<CG, EW>;
@@ -410,6 +435,19 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
+    constexpr int NACC = FP4 ? 1 : 2;  // accumulator buffers
+    if constexpr (FP4) {
+        // block scales = 1.0 everywhere in TMEM columns [256, 512) of both CTAs
+        if (etid >= 0 && etid < EW * 32) {
+            const int fq = warp & 3, fpart = (warp - kEpiWarp0) >> 2;  // EW = 8: 2 warps per lane quadrant
+            for (int c = 0; c < 128; c += 32)
+                tmem_fill_x32(tmem_base + ((uint32_t)(fq * 32) << 16) + kSfCol + (uint32_t)(fpart * 128 + c),
+                              0x7F7F7F7Fu);
+        }
+        tc_fence_before();
+        if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+        tc_fence_after();
+    }
 
     const int nkb = p.num_k_blocks;
     const TileWalk walk{cluster, n_clusters, p.n_full, nkb};
@@ -495,7 +533,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     } else if (warp == 1) {
         // ================= MMA issuer =================
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_i8(C::MMA_M, C::MMA_N);
+            constexpr uint32_t idesc = mma_idesc<CG, FP4>(C::MMA_M, C::MMA_N);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
@@ -514,16 +552,16 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 #pragma unroll
                     for (int k = 0; k < kBK / 32; ++k) {
                         // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
-                        umma_i8<CG>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                        mma_step<CG, FP4>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, tmem_base, (kb | k) != 0 ? 1u : 0u);
                     }
                     umma_commit<CG>(empty_bar(s));  // frees the smem slot (both CTAs)
                     if (++s == ST) { s = 0; ph ^= 1u; }
                 }
                 umma_commit<CG>(tfull_bar(acc));  // accumulator ready (both CTAs)
                 if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 1] = clock64();
-                if (++acc == 2) { acc = 0; aph ^= 1u; }
+                if (++acc == NACC) { acc = 0; aph ^= 1u; }
             }
-            if (has_tail) mma_tail<CG, ST>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
+            if (has_tail) mma_tail<CG, ST, FP4>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
         }
     } else if (PACE && warp == C::PACER_WARP) {
         // ================= pacer =================
@@ -572,6 +610,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         // one tile's epilogue, or of one column slice [c0, c0 + W) of a split
         // tail tile: N mode -- the slice's accumulator in TMEM columns [0, W);
         // K mode -- this unit's full-width partial plus the other units' ones
+        int cpar = 0;
         auto epi_tile = [&](const int t, auto tail_tag) {
             constexpr int TAIL = decltype(tail_tag)::value;  // 0 whole tile, 1 N slice, 2 K-split owner
             const int c0 = TAIL ? tail_c * tail_we : 0;       // first tile column of this epilogue
@@ -580,7 +619,10 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             const int2 tile = p.tiles[t];
             const bool diag = tile.x == tile.y;
             const int i = tile.x * C::TS + (int)rank * 128 + row_local;
-            ColS* const cols = colbuf + acc * C::TS;   // this tile's column marginals
+            // this tile's column marginals, double-buffered by tile parity: a fast
+            // warp stages the next tile's while slow ones still read this one
+            ColS* const cols = colbuf + cpar * C::TS;
+            cpar ^= 1;
             ColS Arow{};
             RowQ AQ{0, 0, 0};
             bool use_table = false;
@@ -624,6 +666,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 uint32_t r[16];
                 tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
                 tmem_ld_wait(r);
+                acc_to_counts<FP4>(r);
                 if constexpr (TAIL == 2) {  // + the other K ranges (integer adds: exact in any order)
                     const int u0 = (t - p.n_full) * p.tail_split;
                     const size_t off = ((size_t)((tc0 + col0) / 16) * 128 + row_local) * 16;
@@ -673,7 +716,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 named_barrier_sync(3, EW * 32);
                 if (etid == 0) atomicAdd_system(p.row_done + tile.x, 1u);
             }
-            if (++acc == 2) { acc = 0; aph ^= 1u; }
+            if (++acc == NACC) { acc = 0; aph ^= 1u; }
         };
         // per-cluster timeline (globaltimer ns): start, main tiles done, tail done
         long long* const ctrace = (p.trace && rank == 0 && etid == 0) ? p.trace + 256 + cluster * 4 : nullptr;
@@ -693,6 +736,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 uint32_t r[16];
                 tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + col0), r);
                 tmem_ld_wait(r);
+                acc_to_counts<FP4>(r);
                 uint4* dst = reinterpret_cast<uint4*>(dst_base + ((size_t)(col0 / 16) * 128 + row_local) * 16);
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4)
@@ -735,9 +779,9 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 
 // ---------------------------------------------------------------- launch
 
-template <int CG, int OUT, int MODE, int ST, int EW, bool PACE>
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE, bool FP4>
 cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream) {
-    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW, PACE>;
+    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW, PACE, FP4>;
     constexpr uint32_t smem = SmemLayout<CG, ST>::request;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -63,14 +63,18 @@ constexpr int kPaceStride = 8;          // u32 per cluster slot (one 32-B sector
 constexpr int kPaceMaxClusters = 256;
 constexpr int kTailMaxUnits = 148;      // split tail units (<= clusters): flag pairs and partial slots
 constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
+constexpr long long kFp4MaxN = 1ll << 24;    // e2m1 operands: fp32 accumulators exact below 2^24
 
-cudaError_t launch_gram_mi(int cg, int out_kind, int mode, int stages, int epi_warps, const CUtensorMap& tmap,
-                           const GramMiParams& p, int num_sms, cudaStream_t stream);
+// fp4: operand X holds e2m1 nibbles (kind::mxf4 build, cg == 2 only), else int8 bytes
+cudaError_t launch_gram_mi(int cg, bool fp4, int out_kind, int mode, int stages, int epi_warps,
+                           const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream);
 int gram_mi_tile_size(int cg);
 
+// fp4: write X as e2m1 nibbles (2 rows per byte, ld = bytes per column row
+// band = N_pad / 2), else int8 bytes (ld = N_pad)
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
                                  int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,
-                                 ColStat* colstat, long long* xlogx, int2* blkrange, int num_sms,
+                                 ColStat* colstat, long long* xlogx, int2* blkrange, bool fp4, int num_sms,
                                  cudaStream_t stream);
 
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,

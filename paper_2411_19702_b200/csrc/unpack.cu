@@ -2,7 +2,8 @@
 //
 // Input is the reference's BinaryMatrix.words layout (binmat.py:3-6,57-97):
 // (m, nw) uint64, column-major, bit r of word w = row 64w + r, padding zero.
-// Output X holds X[c][r] = bit r of column c as 0/1 bytes in a k-blocked
+// Output X holds X[c][r] = bit r of column c as 0/1 bytes (int8 operand) or
+// as e2m1 nibbles 0 / 1.0 (fp4 operand, two rows per byte) in a k-blocked
 // K-major layout: [ld/128 k-blocks][m_pad columns][128 bytes], so the 128 x 128
 // box the GEMM loads for (k-block, 128 columns) is one contiguous 16 KB chunk
 // (one DRAM page, one TLB entry).  Padding rows / columns are zero, so padded
@@ -104,14 +105,36 @@ __device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* sr
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
 
+// 64 bits -> 32 bytes of e2m1 nibbles (row 2j in the low nibble of byte j,
+// row 2j + 1 in the high one; 1.0 = 0b0010), one STG.256.
+__device__ __forceinline__ uint32_t fp4x8(uint32_t b) {
+    uint32_t e = b & 0x55u, o = (b >> 1) & 0x55u;
+    e = (e | (e >> 1)) & 0x33u;
+    e = (e | (e >> 2)) & 0x0Fu;
+    o = (o | (o >> 1)) & 0x33u;
+    o = (o | (o >> 2)) & 0x0Fu;
+    return (spread4(e) << 1) | (spread4(o) << 5);
+}
+__device__ __forceinline__ void store_fp4_word(int8_t* dst, uint64_t w) {
+    uint32_t q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = fp4x8((uint32_t)(w >> (8 * k)) & 0xFFu);
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(q[0]), "r"(q[1]),
+                 "r"(q[2]), "r"(q[3]), "r"(q[4]), "r"(q[5]), "r"(q[6]), "r"(q[7])
+                 : "memory");
+}
+
+template <bool FP4>
 __global__ void __launch_bounds__(256)
 unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x, int64_t ld,
               int64_t m_pad, ColStat* __restrict__ colstat) {
     __shared__ __align__(16) uint64_t tile[2][kUnpackCols * kUnpackPitch];
+    constexpr int WPK = FP4 ? 4 : 2;           // words per 128-byte k-block row
+    constexpr int KBT = kUnpackWords / WPK;    // k-blocks per tile
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
-    const int64_t wpad = ld / 64;  // words per padded column (even)
     const int64_t nkb = ld / 128;
+    const int64_t wpad = nkb * WPK;            // words per padded column
     const int64_t kb_stride = m_pad * 128;
     const int ld_col = t >> 3;     // loader: column of the group
     const int ld_sub = t & 7;      // loader: 8 words of the tile row
@@ -145,13 +168,20 @@ unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t*
         const uint64_t* buf = tile[i & 1];
 #pragma unroll
         for (int k = 0; k < 8; ++k) cnt += __popcll(buf[ld_col * kUnpackPitch + ld_sub * 8 + k]);
-        const int64_t kb0 = (wbeg + (int64_t)i * kUnpackWords) / 2;
+        const int64_t kb0 = (wbeg + (int64_t)i * kUnpackWords) / WPK;
 #pragma unroll
-        for (int kk = 0; kk < kUnpackWords / 2; kk += 8) {
+        for (int kk = 0; kk < KBT; kk += 8) {
             const int kbl = kk + warp;
-            if (kb0 + kbl < nkb)
-                store_row128(x + (kb0 + kbl) * kb_stride + (c0 + lane) * 128, buf[lane * kUnpackPitch + 2 * kbl],
-                             buf[lane * kUnpackPitch + 2 * kbl + 1]);
+            if (kb0 + kbl < nkb) {
+                int8_t* dst = x + (kb0 + kbl) * kb_stride + (c0 + lane) * 128;
+                const uint64_t* wsrc = buf + lane * kUnpackPitch + WPK * kbl;
+                if constexpr (FP4) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) store_fp4_word(dst + 32 * q, wsrc[q]);
+                } else {
+                    store_row128(dst, wsrc[0], wsrc[1]);
+                }
+            }
         }
         __syncthreads();  // buffer i & 1 is reloaded by issue(i + 2)
     }
@@ -171,7 +201,7 @@ __global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m,
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
                                  int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, long long* xlogx,
-                                 int2* blkrange, int num_sms, cudaStream_t stream) {
+                                 int2* blkrange, bool fp4, int num_sms, cudaStream_t stream) {
     const int fix_s = xlogx_scale(n_rows);
     {
         int64_t work = xlogx ? n_rows + 1 : 0;
@@ -181,11 +211,14 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
         unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, xlogx, n_rows, fix_s, blkrange,
                                                              (xlogx && blkrange) ? (int)(m_pad / 128) : 0);
     }
-    const int64_t wpad = ld / 64;
+    const int64_t wpad = ld / 128 * (fp4 ? 4 : 2);
     const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);
     if (chunks > 65535) return cudaErrorInvalidValue;
-    unpack_kernel<<<dim3((unsigned)(m_pad / kUnpackCols), (unsigned)chunks), 256, 0, stream>>>(words, m, nw, x, ld,
-                                                                                              m_pad, colstat);
+    const dim3 grid((unsigned)(m_pad / kUnpackCols), (unsigned)chunks);
+    if (fp4)
+        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat);
+    else
+        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat);
     int64_t cb = (m_pad + 255) / 256;
     if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
     colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, m_pad, colsum, colstat, fix_s,

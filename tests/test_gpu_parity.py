@@ -147,6 +147,7 @@ KNOB_VARIANTS = [
     {"fixed": 0}, {"fixed": 2}, {"band": 1}, {"band": 3}, {"l2_hint": 0}, {"prefetch": 4},
     {"tail": 0}, {"tail": 0, "pace": 16}, {"tail": 0, "cta_group": 1},
     {"tail": 2}, {"tail": 3}, {"tail": 3, "cta_group": 1}, {"tail": 2, "cta_group": 1}, {"tail": 3, "pace": 16},
+    {"fp4": 0}, {"fp4": 0, "tail": 3}, {"fp4": 0, "pace": 16}, {"fp4": 0, "fixed": 0},
 ]
 
 

@@ -42,7 +42,15 @@ def test_library_exports_every_header_function():
 
 def test_layout_helpers():
     lib = nat.lib()
-    assert lib.mi_kmajor_ld(1) == 128 and lib.mi_kmajor_ld(128) == 128 and lib.mi_kmajor_ld(129) == 256
+    old = nat.get_tuning("fp4")
+    try:
+        nat.set_tuning(fp4=0)  # int8 operand: one byte per row, rows padded to 128
+        assert lib.mi_kmajor_ld(1) == 128 and lib.mi_kmajor_ld(128) == 128 and lib.mi_kmajor_ld(129) == 256
+        nat.set_tuning(fp4=1)  # e2m1 operand: two rows per byte, rows padded to 256
+        assert lib.mi_kmajor_ld(1) == 128 and lib.mi_kmajor_ld(256) == 128 and lib.mi_kmajor_ld(257) == 256
+        assert lib.mi_kmajor_ld((1 << 24) + 1) == (1 << 24) + 128  # fp32-exactness limit: back to int8
+    finally:
+        nat.set_tuning(fp4=old)
     assert lib.mi_kmajor_rows(1) == 256 and lib.mi_kmajor_rows(257) == 512
     assert lib.mi_tile_size() in (128, 256)
     T = -(-10000 // lib.mi_tile_size())

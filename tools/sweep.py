@@ -21,6 +21,7 @@ ap.add_argument("--epi", default="8")
 ap.add_argument("--dtype", default="auto")
 ap.add_argument("--pace", default="-1")
 ap.add_argument("--tail", default="1")
+ap.add_argument("--fp4", default="1")
 a = ap.parse_args()
 ints = lambda s: [int(x) for x in s.split(",")]
 eng = MIEngine.get(0)
@@ -30,22 +31,27 @@ for cfg in ints(a.configs):
     rec = datagen.config_recipe(cfg)
     n, m = rec["n"], rec["m"]
     w = datagen.generate_words_device(rec, dev)
-    prep = eng.prepare(w, n, m)
+    prep, prep_ld = None, None
     dt = {"auto": torch.float64 if datagen.CONFIGS[cfg]["out"] == "float64" else torch.float32,
           "f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[a.dtype]
     out = torch.empty((m, m), dtype=dt, device=dev)
     reps = a.reps or {1: 50, 2: 50, 3: 10, 4: 3, 5: 2}[cfg]
     W = n * m * (m + 1) / 2
-    for cg, pf, hint, band, st, ew, pace, tail in itertools.product(ints(a.cg), ints(a.prefetch), ints(a.l2hint),
-                                                              ints(a.band), ints(a.stages), ints(a.epi), ints(a.pace), ints(a.tail)):
+    for cg, pf, hint, band, st, ew, pace, tail, fp4 in itertools.product(
+            ints(a.cg), ints(a.prefetch), ints(a.l2hint), ints(a.band), ints(a.stages), ints(a.epi), ints(a.pace),
+            ints(a.tail), ints(a.fp4)):
         nat.set_tuning(cta_group=cg, prefetch=pf, l2_hint=hint, band=band, stages=st, epi_warps=ew)
-        for key, val in (("pace", pace), ("tail", tail)):  # newer knobs: absent from older A/B builds
+        for key, val in (("pace", pace), ("tail", tail), ("fp4", fp4)):  # newer knobs: absent from older A/B builds
             try:
                 nat.set_tuning(**{key: val})
             except Exception:
-                assert val == {"pace": -1, "tail": 1}[key], f"this build has no '{key}' knob"
+                assert val == {"pace": -1, "tail": 1, "fp4": 0}[key], f"this build has no '{key}' knob"
         eng._tiles.clear()
         tiles = eng.tiles(m)
+        if prep_ld != eng.layout(n, m):  # operand format follows the knobs (fp4, cta_group)
+            prep = None
+            torch.cuda.empty_cache()
+            prep, prep_ld = eng.prepare(w, n, m), eng.layout(n, m)
         eng.compute(prep, None, dt, tiles=tiles, out=out)
         torch.cuda.synchronize()
         ms = []
@@ -55,7 +61,7 @@ for cfg in ints(a.configs):
             e0.record(); eng.compute(prep, None, dt, tiles=tiles, out=out); e1.record()
             e1.synchronize(); ms.append(e0.elapsed_time(e1))
         best, avg = min(ms), sum(ms) / len(ms)
-        print(json.dumps({"cfg": cfg, "cg": cg, "prefetch": pf, "l2hint": hint, "band": band, "stages": st, "epi_warps": ew, "pace": pace, "tail": tail, "dtype": str(dt).split(".")[-1],
+        print(json.dumps({"cfg": cfg, "cg": cg, "prefetch": pf, "l2hint": hint, "band": band, "stages": st, "epi_warps": ew, "pace": pace, "tail": tail, "fp4": fp4, "dtype": str(dt).split(".")[-1],
                           "ms_avg": round(avg, 4), "ms_min": round(best, 4),
                           "tops_avg": round(2 * W / avg / 1e9, 1)}), flush=True)
     del prep, out, w
