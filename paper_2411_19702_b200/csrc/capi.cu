@@ -56,14 +56,15 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
                        env_int("MI_B200_L2HINT", 1), env_int("MI_B200_BAND", 8),
                        env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
-                       env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1)};
+                       env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
+                       env_int("MI_B200_EVAC", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -535,6 +536,7 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.trace = g_trace;
     int dev = 0;
     MI_CUDA(cudaGetDevice(&dev));
+    p.evac = tuning().evac;
     p.pace = nullptr;
     p.pace_window = pace_window(n_tiles, p.num_k_blocks, info.num_sms);
     if (p.pace_window > 0 && (rc = pace_slots(dev, &p.pace))) return rc;
@@ -729,6 +731,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "tail")) {
         if (value < 0 || value > 3) return fail(MI_ERR_DOMAIN, "tail must be 0 (off), 1 (auto), 2 (slices) or 3 (K ranges)");
         t.tail = value;
+    } else if (!strcmp(key, "evac")) {
+        if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "evac must be 0, 1 or 2");
+        t.evac = value;
     } else if (!strcmp(key, "fp4")) {
         if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "fp4 must be 0 (int8 operands) or 1");
         t.fp4 = value;
@@ -758,6 +763,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "pace")) return t.pace;
     if (!strcmp(key, "tail")) return t.tail;
     if (!strcmp(key, "fp4")) return t.fp4;
+    if (!strcmp(key, "evac")) return t.evac;
     return -1;
 }
 

@@ -311,11 +311,17 @@ struct TileWalk {
 // The split tail unit's producer and MMA loops live out of line: inlined after
 // the main loops they cost ~3% of the main loops' throughput (code layout).
 // Operand format: FP4 = e2m1 nibbles (1.0 = 0b0010) through kind::mxf4 with
-// all block scales 1.0 (E8M0 127, TMEM columns [256, 512)), fp32 accumulators
-// (exact integer counts below 2^24 rows), K = 256 per 128-byte k-block, at
-// twice the kind::i8 rate (tools/micro/mxf4_probe.cu).  The scale factors take
-// TMEM beyond one 256-column accumulator, so FP4 runs single-buffered.
-constexpr uint32_t kSfCol = 256;
+// all block scales 1.0 (E8M0 127), fp32 accumulators (exact integer counts
+// below 2^24 rows), K = 256 per 128-byte k-block, at twice the kind::i8 rate
+// (tools/micro/mxf4_probe.cu).  The scales take TMEM columns [496, 512) (the
+// MMA reads 8 columns of them: probe), so there is room for one 256-column
+// accumulator only.  To overlap the epilogue with the next tile's MMAs anyway,
+// the epilogue first evacuates the accumulator -- 240 columns into the spare
+// TMEM columns [256, 496), the last 16 into registers -- releases it (~10k
+// cycles instead of the ~80k of the whole epilogue), then computes from there.
+constexpr uint32_t kSfCol = 496;
+constexpr uint32_t kSpareCol = 256;
+constexpr int kSpareCols = 240;
 template <int CG, bool FP4>
 __device__ __forceinline__ void mma_step(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t tmem_base, uint32_t acc) {
@@ -438,11 +444,12 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     constexpr int NACC = FP4 ? 1 : 2;  // accumulator buffers
     if constexpr (FP4) {
         // block scales = 1.0 everywhere in TMEM columns [256, 512) of both CTAs
-        if (etid >= 0 && etid < EW * 32) {
-            const int fq = warp & 3, fpart = (warp - kEpiWarp0) >> 2;  // EW = 8: 2 warps per lane quadrant
-            for (int c = 0; c < 128; c += 32)
-                tmem_fill_x32(tmem_base + ((uint32_t)(fq * 32) << 16) + kSfCol + (uint32_t)(fpart * 128 + c),
-                              0x7F7F7F7Fu);
+        if (etid >= 0 && etid < 4 * 32) {  // one warp per TMEM lane quadrant
+            const uint32_t one[16] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                      0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                                      0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+            tmem_st_32x32b_x16(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kSfCol, one);
+            tmem_st_wait();
         }
         tc_fence_before();
         if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -659,13 +666,49 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
             if (tracer && it < 64) p.trace[it * 4 + 2] = clock64();
+            const uint32_t lane_q = (uint32_t)(q * 32) << 16;
+            // Evacuate only when the epilogue is FP64-free: an FP64 epilogue next to
+            // running MMAs is throttled ~23x (r01_micro.md), so FP64-path tiles keep
+            // the accumulator until done and run their epilogue alone.
+            const bool EVAC = FP4 && TAIL == 0 && p.evac != 0 && (OUT == MI_OUT_COUNTS || use_table || p.evac == 2);
+            uint32_t keep[16];  // EVAC: the accumulator columns that do not fit the spare TMEM
+            if (EVAC) {
+#pragma unroll 1
+                for (int c = 0; c < part_cols; c += 16) {
+                    const int col0 = part * part_cols + c;
+                    uint32_t r[16];
+                    tmem_ld_32x32b_x16(tmem_base + lane_q + (uint32_t)col0, r);
+                    tmem_ld_wait(r);
+                    if (col0 < kSpareCols) {
+                        tmem_st_32x32b_x16(tmem_base + lane_q + kSpareCol + (uint32_t)col0, r);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) keep[k] = r[k];
+                    }
+                }
+                tmem_st_wait();
+                // the accumulator is free: the next tile's MMAs start now
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader0);
+            }
 #pragma unroll 1
             for (int c = 0; c < part_cols; c += 16) {
                 const int col0 = part * part_cols + c;   // accumulator column
                 const int j0 = tile.y * C::TS + c0 + col0;
                 uint32_t r[16];
-                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
-                tmem_ld_wait(r);
+                if (EVAC) {
+                    if (col0 < kSpareCols) {
+                        tmem_ld_32x32b_x16(tmem_base + lane_q + kSpareCol + (uint32_t)col0, r);
+                        tmem_ld_wait(r);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) r[k] = keep[k];
+                    }
+                } else {
+                    tmem_ld_32x32b_x16(tmem_base + lane_q + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
+                    tmem_ld_wait(r);
+                }
                 acc_to_counts<FP4>(r);
                 if constexpr (TAIL == 2) {  // + the other K ranges (integer adds: exact in any order)
                     const int u0 = (t - p.n_full) * p.tail_split;
@@ -705,11 +748,13 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                                                         row_ok, vec_ok);
                 }
             }
-            // hand the accumulator back to the MMA warp
+            // hand the accumulator back to the MMA warp (EVAC: done above)
             if (tracer && it < 64) p.trace[it * 4 + 3] = clock64();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            if (!EVAC) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            }
             if (p.row_done) {
                 // publish: this CTA's rows and mirrors of tile (I, J) are in memory
                 __threadfence_system();

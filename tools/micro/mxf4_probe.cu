@@ -50,7 +50,7 @@ __host__ __device__ inline int sw128(int r, int kbyte) {
 
 template <bool FP4>
 __global__ void __launch_bounds__(128, 1) gram_probe(const uint8_t* abits, const uint8_t* bbits, float* out_f,
-                                                      int* out_i, long long* cycles, int reps) {
+                                                      int* out_i, long long* cycles, int reps, int sfw) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint32_t tslot;
@@ -89,14 +89,21 @@ __global__ void __launch_bounds__(128, 1) gram_probe(const uint8_t* abits, const
     const uint32_t tmem = tslot;
     // scale factors: columns 256..511 of every lane = 0x7F (E8M0 1.0)
     if (FP4) {
-        for (int c = 256; c < 512; c += 32) tmem_st_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, 0x7F7F7F7Fu);
+        for (int c = 256; c < 512; c += 32) tmem_st_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, 0x80808080u);
+        // sfw columns of 1.0 at SFA (256) and SFB (384), 2.0 elsewhere: exact results <=> the MMA reads
+        // no more than sfw columns of scales
+        for (int c = 0; c < sfw; ++c) {
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + 256 + c), "r"(0x7F7F7F7Fu) : "memory");
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + ((uint32_t)(warp * 32) << 16) + 384 + c), "r"(0x7F7F7F7Fu) : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (threadIdx.x == 0) {
         const uint32_t idesc = FP4 ? idesc_mxf4(M, N) : umma_idesc_i8(M, N);
-        const uint32_t sfa = tmem + 256, sfb = tmem + 320;
+        const uint32_t sfa = tmem + 256, sfb = tmem + 384;
         long long t0 = clock64();
         for (int rep = 0; rep < reps; ++rep) {
             for (int kb = 0; kb < KB; ++kb) {
@@ -153,7 +160,21 @@ int main() {
         cudaMemcpy(db, b.data(), b.size(), cudaMemcpyHostToDevice);
         auto kern = fp4 ? gram_probe<true> : gram_probe<false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<1, 128, smem>>>(da, db, df, di, dc, 1);
+        for (int sfw = 1; fp4 && sfw <= 64; sfw *= 2) {
+            kern<<<1, 128, smem>>>(da, db, df, di, dc, 1, sfw);
+            cudaDeviceSynchronize();
+            std::vector<float> t(M * N);
+            cudaMemcpy(t.data(), df, M * N * 4, cudaMemcpyDeviceToHost);
+            long bad = 0;
+            for (int i = 0; i < M; ++i)
+                for (int j = 0; j < N; ++j) {
+                    int ref = 0;
+                    for (int k = 0; k < K; ++k) ref += a[i * K + k] & b[j * K + k];
+                    bad += t[i * N + j] != (float)ref;
+                }
+            printf("  mxf4 with %d scale column(s) of 1.0 at SFA and SFB: %ld mismatches\n", sfw, bad);
+        }
+        kern<<<1, 128, smem>>>(da, db, df, di, dc, 1, 128);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("%s: %s\n", fp4 ? "mxf4" : "i8", cudaGetErrorString(e)); return 1; }
         std::vector<float> of(M * N);
@@ -174,7 +195,7 @@ int main() {
         printf("%s correctness: K=%d, %ld mismatches of %d\n", fp4 ? "mxf4" : "i8", K, bad, M * N);
         // throughput: all SMs, garbage smem (abits = nullptr skips staging)
         const int reps = 2000;
-        kern<<<148, 128, smem>>>(nullptr, nullptr, nullptr, nullptr, dc, reps);
+        kern<<<148, 128, smem>>>(nullptr, nullptr, nullptr, nullptr, dc, reps, 128);
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("throughput run: %s\n", cudaGetErrorString(e)); return 1; }
         std::vector<long long> cyc(148);
