@@ -28,6 +28,7 @@ import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 from pathlib import Path
 
@@ -37,12 +38,13 @@ sys.path.insert(0, str(ROOT))
 METRIC = "all-pairs binary MI: N·m(m+1)/2 pair-samples/s, % int8 tensor roofline, 1–8 GPU"
 UNIT = "pair-samples/s"
 INT8_NOMINAL_TOPS = 4500.0  # B200 dense int8, datasheet
+FP4_NOMINAL_TOPS = 9000.0   # B200 dense FP4 (tcgen05 kind::mxf4), datasheet
 
 
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -73,6 +75,60 @@ def workload_name(cfg: int, n: int, m: int, out: str) -> str:
 
 
 # ----------------------------------------------------------------- clocks
+class NvmlSampler:
+    """SM clock, power and clock-event reasons sampled through NVML every 2 ms
+    on a background thread for exactly the timed region (the region is short:
+    nvidia-smi's 50 ms loop would see only a sample or two)."""
+
+    def __init__(self, gpu_index: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.samples = []
+        self.stop_flag = threading.Event()
+        self.thread = None
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0,
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        self.stop_flag.set()
+        self.thread.join(timeout=5)
+        nv = self.nv
+        smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                "hw_power_brake_slowdown": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        reasons = sorted({name for _, _, r in self.samples for name, b in bits.items() if r & b})
+        sm = [c for c, _, _ in self.samples]
+        power = [w for _, w, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(sm), "samples_under_load": len(sm), "power_w_max": max(power) if power else None,
+                "source": "NVML every 2 ms over the timed region"}
+
+
+def make_sampler(gpu_index: int):
+    try:
+        return NvmlSampler(gpu_index)
+    except Exception:
+        return ClockSampler(gpu_index)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -263,7 +319,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = make_sampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
     if world > 1:
@@ -294,13 +350,24 @@ def main():
     ops_per_launch = 2.0 * W * (rank_tiles / all_tiles)
     achieved_tops = ops_per_launch / (kern_ms * 1e-3) / 1e12
     peaks = load_peaks()
-    peak = peaks["int8_tops"]
+    fp4 = operand_is_fp4(n)
+    if fp4:  # e2m1 0/1 operands through kind::mxf4: the FP4 tensor peak is the ceiling
+        peak = FP4_NOMINAL_TOPS
+        kernel = ("gram_mi_kernel<2,*,*,6,8,*,fp4> (tcgen05 kind::mxf4 2-SM, e2m1 0/1 operands, unit E8M0 "
+                  "scales, fp32 accumulators = exact counts, fused MI epilogue)")
+        source = ("B200 datasheet dense FP4 (kind::mxf4), 9 PFLOP/s; tools/micro/mxf4_probe.cu measures "
+                  "16382 MACs/clk/SM = 9.53 POP/s at 1965 MHz")
+    else:
+        peak = peaks["int8_tops"]
+        kernel = "gram_mi_kernel<2,*,*> (tcgen05 kind::i8 2-SM + fused MI epilogue)"
+        source = peaks["source"]
     roofline = {
         "bound": "tensor", "achieved": achieved_tops, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved_tops / peak, "traffic": load_traffic(args.config),
-        "kernel": "gram_mi_kernel<2,*,*> (tcgen05 kind::i8 2-SM + fused MI epilogue)",
-        "ops": "int8 tensor ops = 2 x pair-samples (1 MAC per pair-sample)",
-        "peak_source": peaks["source"],
+        "kernel": kernel,
+        "ops": "tensor ops = 2 x pair-samples (1 MAC per pair-sample)",
+        "peak_source": source,
+        "frac_of_int8_datasheet": achieved_tops / INT8_NOMINAL_TOPS,
         "frac_of_2x_measured_bf16": (achieved_tops / peaks["two_x_measured_bf16_tops"]
                                      if "two_x_measured_bf16_tops" in peaks else None),
         "frac_of_cublas_int8": (achieved_tops / peaks["cublas_int8_tops"] if "cublas_int8_tops" in peaks else None),
@@ -329,14 +396,17 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "i8->s32 GEMM + f64 epilogue",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": ("e2m1 0/1 (kind::mxf4) -> f32 exact counts + f64 MI epilogue" if fp4
+                      else "i8->s32 GEMM + f64 epilogue"),
             "data": "synthetic (splitmix64 stream of the reference's datagen, generated on device)",
             "config": {"workload": workload_name(args.config, n, m, out_name), "n_rows": n, "n_cols": m,
                        "output": out_name, "tiles": all_tiles, "tile": 256,
                        "parallelism": f"upper-triangle tiles dealt over {world} GPU(s); words broadcast once",
                        "l2": "flushed between steps (256 MiB write, untimed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": 2 * args.steps,
+            # per step: unpack prologue, unpack, column stats, fused Gram + MI
+            "gpu_launches": 4 * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -396,6 +466,12 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
             "d2h_bytes_per_step": m * m * esz, "ms_per_step": ms, "steps": steps,
             "api": "MIEngine.all_pairs_host (pinned words in, pinned MI out)" if world == 1 else
                    "dispatch.mi_all_pairs_sharded + gather_to_root"}
+
+
+def operand_is_fp4(n_rows: int) -> bool:
+    """The C ABI's operand rule (capi.cu operand_fp4): e2m1 on SM pairs below 2^24 rows."""
+    from paper_2411_19702_b200 import _native as nat
+    return nat.get_tuning("fp4") == 1 and nat.get_tuning("cta_group") == 2 and n_rows < (1 << 24)
 
 
 def load_peaks() -> dict:
