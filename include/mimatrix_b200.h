@@ -54,9 +54,15 @@ const char* mi_last_error(void);
 int mi_device_info(int device, int* num_sms, int* cc_major, int* cc_minor);
 
 /* ---- layout helpers (host only, no device needed) ---- */
-/* padded row count N_pad of the K-major operand (bytes per operand row).
- * The operand is stored k-blocked: [N_pad/128][m_pad][128] int8, i.e. byte
- * r of column c lives at ((r/128) * m_pad + c) * 128 + r % 128. */
+/* bytes per operand row ("ld") of the K-major operand written by
+ * mi_unpack_colsum and read by mi_gram_mi.  The operand is stored k-blocked,
+ * [ld/128][m_pad][128 bytes].  Format (fixed by n_rows and the "fp4" /
+ * "cta_group" knobs, which must not change between the two calls):
+ *   e2m1 (default: n_rows < 2^24, SM-pair tiles): row r of column c is the
+ *     nibble (r % 2) of byte ((r/256) * m_pad + c) * 128 + (r % 256) / 2,
+ *     0 or 1.0 (0b0010); ld = roundup(n_rows, 256) / 2;
+ *   int8 (otherwise): byte ((r/128) * m_pad + c) * 128 + r % 128 is 0 or 1;
+ *     ld = roundup(n_rows, 128). */
 int64_t mi_kmajor_ld(int64_t n_rows);
 /* padded column count m_pad (operand rows, multiple of the tile size) */
 int64_t mi_kmajor_rows(int64_t n_cols);
