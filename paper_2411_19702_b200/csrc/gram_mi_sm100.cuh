@@ -205,6 +205,34 @@ __device__ __forceinline__ void store32(int32_t* p, const int32_t* v) {
                  : "memory");
 }
 
+// Output stores with an L2 eviction-priority hint (experiments: debug bit 8 =
+// evict_first for the output, so it does not push operand lines out of L2).
+__device__ __forceinline__ void store32h(double* p, const double* v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                 "l"(__double_as_longlong(v[0])), "l"(__double_as_longlong(v[1])), "l"(__double_as_longlong(v[2])),
+                 "l"(__double_as_longlong(v[3])), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void store32h(float* p, const float* v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void store32h(int32_t* p, const int32_t* v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st1h(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st1h(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st1h(int32_t* p, int32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
 // The tile row's fixed-point marginals (table path).
 struct RowQ {
     int v, nmv;      // v_i, N - v_i
@@ -271,17 +299,30 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
     }
     if (!row_ok) return;
     // 2) mirror tile: row j, column i (coalesced across the warp)
+    const bool hint = (p.debug & 8) != 0;
+    const uint64_t pol = hint ? l2_policy_evict_first() : 0ull;
     if (!DIAG && !(p.debug & 2)) {
+        if (hint) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (j0 + k < m) out[(int64_t)(j0 + k) * ld + i] = v[k];
+            for (int k = 0; k < 16; ++k)
+                if (j0 + k < m) st1h(out + (int64_t)(j0 + k) * ld + i, v[k], pol);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (j0 + k < m) out[(int64_t)(j0 + k) * ld + i] = v[k];
+        }
     }
     // 3) direct tile: row i, columns j0 .. j0+15
     if (p.debug & 4) return;
     T* dst = out + (int64_t)i * ld + j0;
     if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0 && j0 + 15 < m) {
+        if (hint) {
 #pragma unroll
-        for (int k = 0; k < 16; k += 32 / (int)sizeof(T)) store32(dst + k, v + k);
+            for (int k = 0; k < 16; k += 32 / (int)sizeof(T)) store32h(dst + k, v + k, pol);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; k += 32 / (int)sizeof(T)) store32(dst + k, v + k);
+        }
         return;
     }
 #pragma unroll
@@ -556,10 +597,13 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_sw128_kmajor(sA + s * kStageHalfBytes);
                     const uint64_t bdesc = umma_desc_sw128_kmajor(sB + s * kStageHalfBytes);
+                    if (!(p.debug & 16)) {  // debug 16: data movement only (no MMAs)
 #pragma unroll
-                    for (int k = 0; k < kBK / 32; ++k) {
-                        // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
-                        mma_step<CG, FP4>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, tmem_base, (kb | k) != 0 ? 1u : 0u);
+                        for (int k = 0; k < kBK / 32; ++k) {
+                            // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
+                            mma_step<CG, FP4>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, tmem_base,
+                                              (kb | k) != 0 ? 1u : 0u);
+                        }
                     }
                     umma_commit<CG>(empty_bar(s));  // frees the smem slot (both CTAs)
                     if (++s == ST) { s = 0; ph ^= 1u; }

@@ -28,8 +28,9 @@ struct GramMiParams {
     int include_diagonal;
     int prefetch_dist;      // k-blocks of L2 prefetch ahead of the TMA ring (0 = off)
     int l2_hint;            // 0 normal, 1 evict_last, 2 evict_first for operand loads
-    int debug;              // experiments only: 1 = compute but skip the output stores, 2 = skip the
-                            // mirror stores, 4 = skip the direct stores
+    int debug;              // experiments only (bit mask): 1 = compute but skip the output stores,
+                            // 2 = skip the mirror stores, 4 = skip the direct stores, 8 = L2
+                            // evict_first hint on the output stores, 16 = no MMAs (data movement only)
     long long* trace;       // experiments only: per-tile timestamps of cluster 0 (or nullptr)
     unsigned long long rcp; // fixed point: round(2^(62 + nb) / N), nb = bit length of N
     int off0;               // fixed point: -(nb - 2) - s
