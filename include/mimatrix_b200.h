@@ -38,6 +38,7 @@ extern "C" {
 #define MI_ERR_CONSISTENCY 3 /* ConsistencyError */
 #define MI_ERR_CUDA 4        /* device / driver failure (MiMatrixError) */
 #define MI_ERR_UNSUPPORTED 5 /* not an sm_100 device, or no device   */
+#define MI_ERR_FORMAT 6      /* FormatError (a malformed BMI1 file)  */
 
 /* engine modes (engine.py:28, EngineConfig.mode) */
 #define MI_MODE_EXACT 0
@@ -112,6 +113,20 @@ int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, 
 /* binmat.column_sums(matrix) */
 int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, uint64_t* h_out,
                         int device);
+/* ---- ingest: the BMI1 packed container (io.py:1-16, read_bmi io.py:92-116) ----
+ * "BMI1", n_rows (u64 LE), n_cols (u64 LE), then n_cols columns of
+ * ceil(n_rows/64) little-endian words -- byte for byte the words layout, so
+ * the payload goes to the device as is.
+ * mi_bmi_header validates the header and the payload length (MI_ERR_FORMAT,
+ * with read_bmi's messages) and returns the shape. */
+int mi_bmi_header(const char* path, int64_t* n_rows, int64_t* n_cols);
+/* Stream the payload into d_words (n_cols x ceil(n_rows/64) uint64 on the
+ * current device) through pinned double-buffered staging, file reads
+ * overlapping the H2D copies on `stream`; nonzero padding bits past row
+ * n_rows - 1 are rejected (MI_ERR_FORMAT) like read_bmi.  Returns after the
+ * last copy completed. */
+int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_cols, void* stream);
+
 /* Tuning knobs (process-wide): "cta_group" (2 = 256x256 tiles on an SM pair,
  * 1 = 128x128 on one SM), "prefetch" (L2 prefetch distance in k-blocks),
  * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per

@@ -13,7 +13,7 @@ import os
 import re
 from pathlib import Path
 
-from .errors import ConsistencyError, DimensionError, DomainError, MiMatrixError, NativeError
+from .errors import ConsistencyError, DimensionError, DomainError, FormatError, MiMatrixError, NativeError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmimatrix_b200.so"
 if os.environ.get("MI_B200_LIB"):  # experiments: A/B another build of the library
@@ -26,6 +26,7 @@ MI_ERR_DOMAIN = 2
 MI_ERR_CONSISTENCY = 3
 MI_ERR_CUDA = 4
 MI_ERR_UNSUPPORTED = 5
+MI_ERR_FORMAT = 6
 
 MI_MODE_EXACT = 0
 MI_MODE_EPSILON = 1
@@ -39,6 +40,7 @@ _ERRORS = {
     MI_ERR_CONSISTENCY: ConsistencyError,
     MI_ERR_CUDA: NativeError,
     MI_ERR_UNSUPPORTED: NativeError,
+    MI_ERR_FORMAT: FormatError,
 }
 
 _i64 = ctypes.c_int64
@@ -64,6 +66,8 @@ SIGNATURES = {
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
     "mi_gram_ones_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_column_sums_host": (_int, [_vp, _i64, _i64, _vp, _int]),
+    "mi_bmi_header": (_int, [ctypes.c_char_p, _vp, _vp]),
+    "mi_bmi_load": (_int, [ctypes.c_char_p, _vp, _i64, _i64, _vp]),
     "mi_set_tuning": (_int, [ctypes.c_char_p, _int]),
     "mi_get_tuning": (_int, [ctypes.c_char_p]),
     "mi_release_workspace": (None, []),

@@ -190,6 +190,14 @@ class MIEngine:
                          out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None) -> torch.Tensor:
         return self.compute(self.prepare(words_dev, n_rows, n_cols), cfg, out_dtype, out=out)
 
+    def all_pairs_bmi(self, path, cfg=None, out_dtype: torch.dtype = torch.float64) -> torch.Tensor:
+        """MI straight from a BMI1 file (the reference's packed container,
+        io.py:1-16): payload streamed to the device, then kernels 1-3."""
+        from .io import read_bmi_device
+
+        words, n_rows, n_cols = read_bmi_device(path, self.device)
+        return self.all_pairs_device(words, n_rows, n_cols, cfg, out_dtype)
+
     def gram_counts(self, words_dev: torch.Tensor, n_rows: int, n_cols: int) -> tuple[torch.Tensor, torch.Tensor]:
         """Debug export for parity: (G11 int32 m x m, column sums int32 m)."""
         prep = self.prepare(words_dev, n_rows, n_cols)
