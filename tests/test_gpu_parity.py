@@ -260,3 +260,38 @@ def test_config_recipes_bit_exact(engine, cfg):
     w = datagen.generate_words_device(rec, engine.device).cpu().numpy().view(np.uint64)
     ref = O.pack_bits(O.generate_config_bits(O.config_recipe(cfg, n, m)))
     assert np.array_equal(w, ref)
+
+
+def _stress_words(n, m, seed):
+    """Columns that stress the float32 epilogue: densities from 1e-4 to
+    1 - 1e-4, exact copies, complements, subsets and near-copies."""
+    rng = np.random.default_rng(seed)
+    dens = np.concatenate([[1e-4, 1e-3, 0.01, 0.5, 0.99, 0.999, 0.9999], rng.uniform(0, 1, m)])[:m]
+    bits = (rng.random((n, m)) < dens[None, :]).astype(np.uint8)
+    for k in range(0, m - 8, 23):
+        bits[:, k + 1] = bits[:, k]                                  # copy
+        bits[:, k + 2] = 1 - bits[:, k]                              # complement
+        bits[:, k + 3] = bits[:, k] & (rng.random(n) < 0.5)          # subset
+        bits[:, k + 4] = bits[:, k] ^ (rng.random(n) < 0.001)        # near copy
+    return O.pack_bits(bits)
+
+
+@pytest.mark.parametrize("n,m", [(20_000, 700), (1_000, 300), (300_000, 260), (4_097, 513)])
+@pytest.mark.parametrize("fixed", [0, 1])
+def test_f32_epilogue_stress(engine, n, m, fixed):
+    """float32 output (fixed=0: the FP64 epilogue on every tile; 1 = adaptive,
+    table path where the column sums allow) stays within the 1e-6 contract of
+    the float64 oracle on adversarial columns, bit-identically symmetric."""
+    from paper_2411_19702_b200 import _native as nat
+
+    words = _stress_words(n, m, seed=n + m)
+    old = nat.get_tuning("fixed")
+    try:
+        nat.set_tuning(fixed=fixed)
+        mi = gpu_mi(engine, words, n, None, torch.float32)
+    finally:
+        nat.set_tuning(fixed=old)
+    ref = O.c_mi_all_pairs(words, n)
+    assert np.array_equal(mi, mi.T)
+    err = float(np.max(np.abs(mi.astype(np.float64) - ref)))
+    assert err < TOL_F32, err
