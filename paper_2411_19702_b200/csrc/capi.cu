@@ -330,6 +330,7 @@ struct Workspace {
     void* tiles = nullptr; size_t tiles_cap = 0;
     void* out = nullptr; size_t out_cap = 0;
     cudaStream_t copy_stream = nullptr;   // D2H of finished row bands
+    cudaEvent_t copy_ev[2] = {nullptr, nullptr};  // the last two D2H copies
     unsigned int* row_done_h = nullptr;   // pinned, mapped: per tile row completion counts
     unsigned int* row_done_d = nullptr;   // device alias of row_done_h
     size_t row_done_cap = 0;
@@ -358,6 +359,8 @@ void release(Workspace& w) {
     w.words_cap = w.x_cap = w.colsum_cap = w.colstat_cap = w.tiles_cap = w.out_cap = 0;
     if (w.stream) cudaStreamDestroy(w.stream), w.stream = nullptr;
     if (w.copy_stream) cudaStreamDestroy(w.copy_stream), w.copy_stream = nullptr;
+    for (auto& e : w.copy_ev)
+        if (e) cudaEventDestroy(e), e = nullptr;
     if (w.row_done_h) cudaFreeHost(w.row_done_h), w.row_done_h = nullptr, w.row_done_d = nullptr;
     w.row_done_cap = 0;
     w.device = -1;
@@ -633,16 +636,34 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     // Stream finished rows to the host while the GEMM continues: rows of tile
     // row b are final once every tile row I <= b is complete (its own tiles
     // and all mirrors landing in it), so copy the completed prefix.
+    // At most two copies in flight: while the link is busy the finished rows
+    // accumulate, so chunks grow (a handful of copies in all; each extra copy
+    // costs ~25 us of engine time, tools/d2h_streams.py), yet the queued one
+    // keeps the copy engine from idling between them.
     const int64_t min_chunk_rows = (int64_t)((16u << 20) / row_bytes) + 1;
     int64_t copied = 0, I = 0;
     bool kernel_done = false;
+    if (!ws->copy_ev[0]) {
+        MI_CUDA(cudaEventCreateWithFlags(&ws->copy_ev[0], cudaEventDisableTiming));
+        MI_CUDA(cudaEventCreateWithFlags(&ws->copy_ev[1], cudaEventDisableTiming));
+    }
+    int issued = 0;
+    auto in_flight = [&]() {
+        int n = 0;
+        for (int k = issued - 2 < 0 ? 0 : issued - 2; k < issued; ++k)
+            if (cudaEventQuery(ws->copy_ev[k & 1]) == cudaErrorNotReady) ++n;
+        return n;
+    };
     while (copied < n_cols) {
         while (I < T && done[I] >= expect[(size_t)I]) ++I;
         int64_t final_rows = I * tile < n_cols ? I * tile : n_cols;
         if (kernel_done) final_rows = n_cols;
-        if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols)) {
+        if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols) &&
+            (kernel_done || in_flight() < 2)) {
             MI_CUDA(cudaMemcpyAsync((char*)h_out + copied * row_bytes, (char*)ws->out + copied * row_bytes,
                                     (size_t)(final_rows - copied) * row_bytes, cudaMemcpyDeviceToHost, ws->copy_stream));
+            MI_CUDA(cudaEventRecord(ws->copy_ev[issued & 1], ws->copy_stream));
+            ++issued;
             if (verbose) {
                 char msg[96];
                 snprintf(msg, sizeof(msg), "D2H rows [%lld, %lld) issued", (long long)copied, (long long)final_rows);
