@@ -138,10 +138,12 @@ TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb) {
 std::mutex g_tail_mu;
 unsigned int* g_tail_flag[64] = {};
 uint32_t* g_tail_part[64] = {};
+cudaEvent_t g_tail_ev[64] = {};  // completion of the last launch that used the slots
 
 int tail_slots(int device, unsigned int** flag, uint32_t** part) {
     std::lock_guard<std::mutex> lk(g_tail_mu);
     if (!g_tail_flag[device]) {
+        MI_CUDA(cudaEventCreateWithFlags(&g_tail_ev[device], cudaEventDisableTiming));
         unsigned int* f = nullptr;
         uint32_t* q = nullptr;
         MI_CUDA(cudaMalloc((void**)&f, (size_t)kTailMaxUnits * 2 * 4));
@@ -550,8 +552,14 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.tail_epi = tp.epi;
     p.tail_flag = nullptr;
     p.tail_part = nullptr;
+    // The K-range tail's flags and partial slots are one per device: launches
+    // that use them are chained across streams (the next waits for the last)
+    // so concurrent callers on different streams cannot mix their partials.
+    std::unique_lock<std::mutex> tail_lk(g_tail_mu, std::defer_lock);
     if (tp.kmode) {
         if ((rc = tail_slots(dev, &p.tail_flag, &p.tail_part))) return rc;
+        tail_lk.lock();
+        MI_CUDA(cudaStreamWaitEvent(stream, g_tail_ev[dev], 0));
         MI_CUDA(cudaMemsetAsync(p.tail_flag, 0, (size_t)(n_tiles - tp.n_full) * 2 * 4, stream));
     }
     fixed_point_consts(n_rows, &p.rcp, &p.off0);
@@ -564,6 +572,7 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
     MI_CUDA(launch_gram_mi(cta_group(), operand_fp4(n_rows), out_kind, eff_mode, tuning().stages, tuning().epi_warps,
                            tm, p, info.num_sms, stream));
+    if (tp.kmode) MI_CUDA(cudaEventRecord(g_tail_ev[dev], stream));
     return MI_OK;
 }
 

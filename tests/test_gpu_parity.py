@@ -295,3 +295,38 @@ def test_f32_epilogue_stress(engine, n, m, fixed):
     assert np.array_equal(mi, mi.T)
     err = float(np.max(np.abs(mi.astype(np.float64) - ref)))
     assert err < TOL_F32, err
+
+
+def test_concurrent_streams_with_k_range_tails(engine):
+    """Two host threads launch on two streams at once; both shapes use the
+    K-range tail (shared per-device partial slots), which the C ABI chains
+    across streams: every result equals its serial result."""
+    import threading
+
+    from paper_2411_19702_b200 import _native as nat
+
+    shapes = [(40_000, 3000, 1), (30_000, 3000, 2)]  # 78 tiles: 4 tail tiles, K-range split
+    data = []
+    for n, m, seed in shapes:
+        words = O.pack_bits(rand_bits(np.random.default_rng(seed), n, m, 0.4))
+        dev = engine.upload(words)
+        data.append((n, m, dev, engine.all_pairs_device(dev, n, m).cpu().numpy()))
+    assert nat.get_tuning("tail") in (1, 3)
+    results = [None, None]
+
+    def work(k):
+        n, m, dev, _ = data[k]
+        s = torch.cuda.Stream(engine.device)
+        with torch.cuda.stream(s):
+            outs = [engine.all_pairs_device(dev, n, m) for _ in range(6)]
+        s.synchronize()
+        results[k] = [o.cpu().numpy() for o in outs]
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for k in range(2):
+        for got in results[k]:
+            assert np.array_equal(got, data[k][3])
