@@ -81,6 +81,11 @@ int64_t mi_num_tiles(int64_t n_cols);
  * tiles_out = NULL to query the count. */
 int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* tiles_out,
                      int64_t capacity);
+/* the column blocks (of mi_tile_size() columns) rank's tiles touch: mask_out[b]
+ * = 1/0 for b < ceil(n_cols / tile); returns the number of marked blocks, or
+ * the block count when mask_out = NULL (8 ranks: half of them, see the
+ * "shard" knob; other world sizes: nearly all). */
+int64_t mi_rank_blocks(int64_t n_cols, int rank, int world, uint8_t* mask_out, int64_t capacity);
 
 /* ---- device-pointer entry points, enqueued on `stream` ---- */
 /* words (m x nw uint64, nw = ceil(n_rows/64)) -> kmajor (k-blocked, m_pad * ld int8),
@@ -88,6 +93,12 @@ int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* til
  * (m_pad int32; padding columns get 0). */
 int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor,
                      int64_t ld, void* d_colstat, int32_t* d_colsum, void* stream);
+/* the same, expanding only the column blocks marked in d_block_mask (device,
+ * one byte per block as from mi_rank_blocks; NULL = all): a rank's share of X.
+ * Statistics of unmarked columns are not meaningful. */
+int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor,
+                            int64_t ld, void* d_colstat, int32_t* d_colsum, const uint8_t* d_block_mask,
+                            void* stream);
 /* Fused G11 + MI over the listed upper-triangle tiles; writes each tile and
  * its mirror into d_out (row-major, pitch ld_out elements). */
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
@@ -136,7 +147,10 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * the tile's column-sum spread), "pace" (L2 pacing window in k-blocks that
  * keeps the SM pairs' K sweeps together: -1 auto (default), 0 off), "tail"
  * (the last partial round of tiles split over the idle SM pairs: 1 auto,
- * default; 0 off; 2 column slices; 3 K ranges).  Also
+ * default; 0 off; 2 column slices; 3 K ranges), "fp4" (1 = e2m1 operands on
+ * kind::mxf4 when N < 2^24, default; 0 = int8), "evac" (e2m1: evacuate the
+ * accumulator before FP64-free epilogues; 1 default, 0 off, 2 always),
+ * "shard" (8 ranks: 1 = column-group pairs, default; 0 = round robin).  Also
  * settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */

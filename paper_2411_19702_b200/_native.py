@@ -60,7 +60,9 @@ SIGNATURES = {
     "mi_tile_size": (_int, []),
     "mi_num_tiles": (_i64, [_i64]),
     "mi_tile_list": (_i64, [_i64, _int, _int, _int, _vp, _i64]),
+    "mi_rank_blocks": (_i64, [_i64, _int, _int, _vp, _i64]),
     "mi_unpack_colsum": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "mi_unpack_colsum_blocks": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
     "mi_gram_mi": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
     "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
@@ -128,6 +130,18 @@ def set_tuning(**kw) -> None:
 
 def get_tuning(key: str) -> int:
     return int(lib().mi_get_tuning(key.encode()))
+
+
+def rank_blocks(n_cols: int, rank: int = 0, world: int = 1):
+    """uint8 mask of the column blocks rank's tiles touch (host-side logic only)."""
+    import numpy as np
+
+    T = int(lib().mi_rank_blocks(n_cols, rank, world, None, 0))
+    check(0 if T > 0 else -T, "mi_rank_blocks")
+    mask = np.zeros(T, dtype=np.uint8)
+    n = int(lib().mi_rank_blocks(n_cols, rank, world, mask.ctypes.data, T))
+    check(0 if n >= 0 else -n, "mi_rank_blocks")
+    return mask
 
 
 def tile_list(n_cols: int, rank: int = 0, world: int = 1, band: int = 0):

@@ -56,7 +56,7 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -64,7 +64,7 @@ Tuning& tuning() {
                        env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
-                       env_int("MI_B200_EVAC", 1)};
+                       env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -321,6 +321,37 @@ std::vector<int32_t> all_tiles(int64_t T, int band, int first = 0) {
     return v;
 }
 
+// A rank's tiles.  Round robin over the banded order (every rank touches
+// nearly every column block), except for 8 ranks ("shard" knob, T >= 8): the
+// column blocks form 4 groups; ranks 0-5 take the 6 off-diagonal group pairs
+// (g, h), ranks 6 and 7 two diagonal groups each ((0,0)+(3,3), (1,1)+(2,2)).
+// Every rank then reads -- and unpacks -- only 2 of the 4 groups (half of X),
+// at a load imbalance of ~4/T (off-diagonal s^2 tiles vs s^2 + s).
+std::vector<int32_t> rank_tiles(int64_t T, int rank, int world, int band) {
+    const std::vector<int32_t> all = all_tiles(T, band);
+    const int64_t total = (int64_t)all.size() / 2;
+    std::vector<int32_t> v;
+    if (world == 8 && T >= 8 && tuning().shard) {
+        auto group = [&](int64_t b) { return (int)((b * 4) / T); };
+        static const int pairs[8][4] = {{0, 1, -1, -1}, {0, 2, -1, -1}, {0, 3, -1, -1}, {1, 2, -1, -1},
+                                        {1, 3, -1, -1}, {2, 3, -1, -1}, {0, 0, 3, 3}, {1, 1, 2, 2}};
+        const int* pr = pairs[rank];
+        for (int64_t k = 0; k < total; ++k) {
+            const int gi = group(all[2 * k]), gj = group(all[2 * k + 1]);
+            if ((gi == pr[0] && gj == pr[1]) || (pr[2] >= 0 && gi == pr[2] && gj == pr[3])) {
+                v.push_back(all[2 * k]);
+                v.push_back(all[2 * k + 1]);
+            }
+        }
+        return v;
+    }
+    for (int64_t g = rank; g < total; g += world) {
+        v.push_back(all[2 * g]);
+        v.push_back(all[2 * g + 1]);
+    }
+    return v;
+}
+
 // Grow-only device workspace for the host-buffer entry points.
 struct Workspace {
     int device = -1;
@@ -383,8 +414,8 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
     MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
                                  (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
-                                 blkrange_ptr(ws.colstat, n_rows, n_cols), operand_fp4(n_rows), info.num_sms,
-                                 ws.stream));
+                                 blkrange_ptr(ws.colstat, n_rows, n_cols), operand_fp4(n_rows), nullptr,
+                                 mi_tile_size(), info.num_sms, ws.stream));
     *ld_out = ld;
     *m_pad_out = m_pad;
     return MI_OK;
@@ -462,22 +493,37 @@ int64_t mi_tile_list(int64_t n_cols, int rank, int world, int band, int32_t* til
         return -fail(MI_ERR_DOMAIN, "bad rank %d of world %d", rank, world);
     if (band <= 0) band = tile_band();
     const int64_t T = tiles_per_side(n_cols);
-    std::vector<int32_t> all = all_tiles(T, band);
-    const int64_t total = (int64_t)all.size() / 2;
-    int64_t count = 0;
-    for (int64_t g = rank; g < total; g += world) {
-        if (tiles_out) {
-            if (count >= capacity) return -fail(MI_ERR_DIMENSION, "tile buffer too small");
-            tiles_out[2 * count] = all[2 * g];
-            tiles_out[2 * count + 1] = all[2 * g + 1];
-        }
-        ++count;
+    const std::vector<int32_t> mine = rank_tiles(T, rank, world, band);
+    const int64_t count = (int64_t)mine.size() / 2;
+    if (tiles_out) {
+        if (count > capacity) return -fail(MI_ERR_DIMENSION, "tile buffer too small");
+        memcpy(tiles_out, mine.data(), mine.size() * sizeof(int32_t));
     }
     return count;
 }
 
+int64_t mi_rank_blocks(int64_t n_cols, int rank, int world, uint8_t* mask_out, int64_t capacity) {
+    if (n_cols < 1) return -fail(MI_ERR_DIMENSION, "n_cols must be >= 1");
+    if (world < 1 || rank < 0 || rank >= world)
+        return -fail(MI_ERR_DOMAIN, "bad rank %d of world %d", rank, world);
+    const int64_t T = tiles_per_side(n_cols);
+    if (!mask_out) return T;
+    if (capacity < T) return -fail(MI_ERR_DIMENSION, "mask buffer too small");
+    memset(mask_out, 0, (size_t)T);
+    const std::vector<int32_t> mine = rank_tiles(T, rank, world, tile_band());
+    for (size_t k = 0; k < mine.size(); ++k) mask_out[mine[k]] = 1;
+    int64_t used = 0;
+    for (int64_t b = 0; b < T; ++b) used += mask_out[b];
+    return used;
+}
+
 int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor, int64_t ld,
                      void* d_colstat, int32_t* d_colsum, void* stream) {
+    return mi_unpack_colsum_blocks(d_words, n_rows, n_cols, d_kmajor, ld, d_colstat, d_colsum, nullptr, stream);
+}
+
+int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor, int64_t ld,
+                            void* d_colstat, int32_t* d_colsum, const uint8_t* d_block_mask, void* stream) {
     int rc = check_shape(n_rows, n_cols);
     if (rc) return rc;
     if (ld < mi_kmajor_ld(n_rows) || ld % 128)
@@ -489,8 +535,8 @@ int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, in
     if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
     MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
                                  (ColStat*)d_colstat, xlogx_ptr(d_colstat, n_rows, n_cols),
-                                 blkrange_ptr(d_colstat, n_rows, n_cols), operand_fp4(n_rows), info.num_sms,
-                                 (cudaStream_t)stream));
+                                 blkrange_ptr(d_colstat, n_rows, n_cols), operand_fp4(n_rows), d_block_mask,
+                                 mi_tile_size(), info.num_sms, (cudaStream_t)stream));
     return MI_OK;
 }
 
@@ -845,6 +891,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "tail")) {
         if (value < 0 || value > 3) return fail(MI_ERR_DOMAIN, "tail must be 0 (off), 1 (auto), 2 (slices) or 3 (K ranges)");
         t.tail = value;
+    } else if (!strcmp(key, "shard")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "shard must be 0 (round robin) or 1 (column groups)");
+        t.shard = value;
     } else if (!strcmp(key, "evac")) {
         if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "evac must be 0, 1 or 2");
         t.evac = value;
@@ -878,6 +927,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "tail")) return t.tail;
     if (!strcmp(key, "fp4")) return t.fp4;
     if (!strcmp(key, "evac")) return t.evac;
+    if (!strcmp(key, "shard")) return t.shard;
     return -1;
 }
 

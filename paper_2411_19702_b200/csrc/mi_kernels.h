@@ -73,12 +73,13 @@ cudaError_t launch_gram_mi(int cg, bool fp4, int out_kind, int mode, int stages,
                            const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream);
 int gram_mi_tile_size(int cg);
 
-// fp4: write X as e2m1 nibbles (2 rows per byte, ld = bytes per column row
+// block_mask (device, one byte per tile-size column block, or nullptr = all):
+// expand only the marked blocks of X (a rank's share); fp4: write X as e2m1 nibbles (2 rows per byte, ld = bytes per column row
 // band = N_pad / 2), else int8 bytes (ld = N_pad)
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
                                  int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,
-                                 ColStat* colstat, long long* xlogx, int2* blkrange, bool fp4, int num_sms,
-                                 cudaStream_t stream);
+                                 ColStat* colstat, long long* xlogx, int2* blkrange, bool fp4,
+                                 const uint8_t* block_mask, int tile, int num_sms, cudaStream_t stream);
 
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,
                                   const uint64_t* col_threshold, const uint8_t* col_kind,

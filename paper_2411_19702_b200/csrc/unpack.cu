@@ -127,7 +127,8 @@ __device__ __forceinline__ void store_fp4_word(int8_t* dst, uint64_t w) {
 template <bool FP4>
 __global__ void __launch_bounds__(256)
 unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x, int64_t ld,
-              int64_t m_pad, ColStat* __restrict__ colstat) {
+              int64_t m_pad, ColStat* __restrict__ colstat, const uint8_t* __restrict__ block_mask, int tile_cols) {
+    if (block_mask && !block_mask[(int64_t)blockIdx.x * kUnpackCols / tile_cols]) return;  // not this rank's block
     __shared__ __align__(16) uint64_t tile[2][kUnpackCols * kUnpackPitch];
     constexpr int WPK = FP4 ? 4 : 2;           // words per 128-byte k-block row
     constexpr int KBT = kUnpackWords / WPK;    // k-blocks per tile
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m,
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
                                  int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, long long* xlogx,
-                                 int2* blkrange, bool fp4, int num_sms, cudaStream_t stream) {
+                                 int2* blkrange, bool fp4, const uint8_t* block_mask, int tile, int num_sms,
+                                 cudaStream_t stream) {
     const int fix_s = xlogx_scale(n_rows);
     {
         int64_t work = xlogx ? n_rows + 1 : 0;
@@ -216,9 +218,9 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
     if (chunks > 65535) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)(m_pad / kUnpackCols), (unsigned)chunks);
     if (fp4)
-        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat);
+        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile);
     else
-        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat);
+        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile);
     int64_t cb = (m_pad + 255) / 256;
     if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
     colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, m_pad, colsum, colstat, fix_s,

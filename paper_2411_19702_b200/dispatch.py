@@ -4,9 +4,10 @@ The output tiles (I <= J) of the MI matrix are independent and all cost the
 same (K = N), so the path shards with no data-path reduction
 (SURVEY 8(e)): rank 0 holds the packed words; ONE broadcast sends them to
 every rank (NCCL over NVLink, bit-packed so it is 1/8 of the int8 operand);
-each rank unpacks its own copy and computes the tiles the C ABI's
-``mi_tile_list(m, rank, world)`` deals it, writing each tile and its mirror
-into its local output.  The MI matrix stays sharded; ``gather_to_root``
+each rank unpacks the column blocks its tiles touch (``mi_rank_blocks``: half
+of them at 8 ranks, whose tiles are dealt as column-group pairs) and computes
+the tiles the C ABI's ``mi_tile_list(m, rank, world)`` deals it, writing each
+tile and its mirror into its local output.  The MI matrix stays sharded; ``gather_to_root``
 assembles it on request.
 
 Everything here is plain torch.distributed plumbing around two callables,
@@ -113,7 +114,7 @@ def mi_all_pairs_sharded(engine, words: torch.Tensor | None, n_rows: int, n_cols
         out.zero_()
 
     def compute(w, tiles, o):
-        prep = engine.prepare(w, n_rows, n_cols)
+        prep = engine.prepare(w, n_rows, n_cols, rank, world)  # only this rank's column blocks
         engine.compute(prep, cfg, out_dtype, tiles=engine.tiles(n_cols, rank, world), out=o)
 
     tiles = run_sharded(words, n_rows, n_cols, compute, out, engine.device, group)

@@ -130,7 +130,7 @@ class MIEngine:
 
     def tiles(self, n_cols: int, rank: int = 0, world: int = 1) -> torch.Tensor:
         # the list depends on the tile size (cta_group) and order (band) knobs
-        key = (n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("band"))
+        key = (n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("band"), nat.get_tuning("shard"))
         t = self._tiles.get(key)
         if t is None:
             host = nat.tile_list(n_cols, rank, world)
@@ -144,9 +144,11 @@ class MIEngine:
         host = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))
         return host.to(self.device, non_blocking=False)
 
-    def prepare(self, words_dev: torch.Tensor, n_rows: int, n_cols: int) -> Prepared:
-        """Kernel 1: unpack the packed columns to the K-major int8 operand and
-        count ones per column (binmat.column_sums)."""
+    def prepare(self, words_dev: torch.Tensor, n_rows: int, n_cols: int,
+                rank: int = 0, world: int = 1) -> Prepared:
+        """Kernel 1: unpack the packed columns to the K-major operand and
+        count ones per column (binmat.column_sums).  With world > 1 only the
+        column blocks of rank's tiles are expanded (mi_rank_blocks)."""
         nw = n_words(n_rows)
         if words_dev.device != self.device or words_dev.dtype not in (torch.int64, torch.uint64):
             raise DimensionError("words must be a 64-bit tensor on the engine's device")
@@ -156,9 +158,18 @@ class MIEngine:
         x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
         colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
         colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_rows, n_cols)),), dtype=torch.uint8, device=self.device)
-        nat.check(nat.lib().mi_unpack_colsum(words_dev.data_ptr(), n_rows, n_cols, x.data_ptr(), ld,
-                                             colstat.data_ptr(), colsum.data_ptr(), _stream_ptr(self.device)),
-                  "mi_unpack_colsum")
+        mask = None
+        if world > 1:
+            key = ("blocks", n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("shard"))
+            mask = self._tiles.get(key)
+            if mask is None:
+                mask = torch.from_numpy(nat.rank_blocks(n_cols, rank, world)).to(self.device)
+                self._tiles[key] = mask
+        nat.check(nat.lib().mi_unpack_colsum_blocks(words_dev.data_ptr(), n_rows, n_cols, x.data_ptr(), ld,
+                                                    colstat.data_ptr(), colsum.data_ptr(),
+                                                    mask.data_ptr() if mask is not None else None,
+                                                    _stream_ptr(self.device)),
+                  "mi_unpack_colsum_blocks")
         return Prepared(n_rows, n_cols, ld, m_pad, x, colsum, colstat)
 
     def compute(self, prep: Prepared, cfg=None, out_dtype: torch.dtype = torch.float64,

@@ -84,3 +84,30 @@ def test_two_rank_sharded_gather_matches_single(n, m, cfg_id, dtype):
     root = [r for r in results if r[0] == "ok"][0]
     assert root[1], "2-rank gathered matrix differs from the single-process result"
     assert sum(r[2] for r in results) >= 1
+
+
+@pytest.mark.parametrize("n,m,dtype", [(20_000, 2_300, "float64"), (6_000, 4_100, "float32")])
+def test_eight_rank_shares_in_one_process(engine, n, m, dtype):
+    """The 8-rank column-group dealing with per-rank partial unpacks
+    (mi_rank_blocks + mi_unpack_colsum_blocks), run rank by rank in one
+    process: the shards, zero elsewhere, sum to the 1-rank matrix exactly."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2411_19702_b200 import _native as nat
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    dt = getattr(torch, dtype)
+    rng = np.random.default_rng(m)
+    words = O.pack_bits((rng.random((n, m)) < 0.35).astype(np.uint8))
+    dev = engine.upload(words)
+    full = engine.all_pairs_device(dev, n, m, None, dt)
+    acc = torch.zeros_like(full)
+    T = -(-m // nat.lib().mi_tile_size())
+    for r in range(8):
+        assert int(nat.rank_blocks(m, r, 8).sum()) <= T // 2 + 2
+        prep = engine.prepare(dev, n, m, r, 8)
+        out = torch.zeros_like(full)
+        engine.compute(prep, None, dt, tiles=engine.tiles(m, r, 8), out=out)
+        acc += out
+    assert torch.equal(acc, full)
