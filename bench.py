@@ -308,7 +308,7 @@ def main():
     def step(ev_k0=None, ev_k1=None):
         if world > 1:
             dist.broadcast(words_local, src=0)
-        prep = eng.prepare(words_local, n, m)
+        prep = eng.prepare(words_local, n, m, rank, world)  # this rank's column blocks only
         if ev_k0 is not None:
             ev_k0.record(stream)
         eng.compute(prep, cfg, out_dtype, tiles=tiles, out=out)
