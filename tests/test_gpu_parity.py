@@ -330,3 +330,21 @@ def test_concurrent_streams_with_k_range_tails(engine):
     for k in range(2):
         for got in results[k]:
             assert np.array_equal(got, data[k][3])
+
+
+@pytest.mark.parametrize("mode,diag,dtype", [("exact", False, "float64"), ("epsilon", True, "float64"),
+                                             ("epsilon", False, "float32"), ("exact", True, "float32")])
+def test_config_variants_with_full_rounds(engine, mode, diag, dtype):
+    """m = 3000 (78 tiles: a full round of 74 pairs, so main-loop tiles run
+    the evacuated epilogue, plus a split tail) in every EngineConfig variant."""
+    n, m = 5_000, 3_000
+    rng = np.random.default_rng(31)
+    words = O.pack_bits(rand_bits(rng, n, m, 0.5))
+    dt = getattr(torch, dtype)
+    mi = gpu_mi(engine, words, n, cfg_of(mode, 1e-9, diag), dt)
+    ref = O.c_mi_all_pairs(words, n, mode=mode, epsilon=1e-9, include_diagonal=diag)
+    assert np.array_equal(mi, mi.T)
+    tol = TOL_F64 if dtype == "float64" else TOL_F32
+    assert float(np.max(np.abs(mi.astype(np.float64) - ref))) < tol
+    if not diag:
+        assert np.all(np.diagonal(mi) == 0)
