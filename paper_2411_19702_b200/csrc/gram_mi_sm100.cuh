@@ -1,6 +1,6 @@
 // Kernel template of the fused Gram + MI path (instantiated by gram_mi_inst_*.cu).
 #pragma once
-// Kernel 2+3: symmetric upper-triangle int8 Gram on tcgen05 with the mutual-
+// Kernels 2+3: symmetric upper-triangle 0/1 Gram on tcgen05 with the mutual-
 // information epilogue fused onto the TMEM accumulators.
 //
 // Replaces, for one output tile at a time, the reference's
@@ -12,21 +12,24 @@
 // once by the epilogue warps and written out as MI(I,J) and its mirror
 // MI(J,I).
 //
-// Layout: X is the K-major int8 expansion of the bit-packed
-// columns, X[c][r] = bit r of column c, stored k-blocked as
-// [N_pad/128][m_pad][128 bytes] (N_pad % 128 == 0, m_pad % 256 == 0, zero
-// padded) so each 128 x 128 TMA box is one contiguous 16 KB chunk.  Both GEMM
-// operands are row blocks of X.
+// Operand: X holds bit r of column c as an e2m1 nibble
+// (FP4 = true: kind::mxf4, unit block scales, fp32 accumulators -- exact
+// counts below 2^24 rows -- at twice the int8 rate) or as an int8 byte
+// (kind::i8, s32 accumulators), stored k-blocked as [ld/128][m_pad][128 bytes]
+// (m_pad % 256 == 0, zero padded) so each 128 x 128-byte TMA box is one
+// contiguous 16 KB chunk.  Both GEMM operands are row blocks of X.
 //
 // Warp roles (one CTA per SM, persistent over a static tile list):
 //   warp 0            TMA producer (one lane): A = X[rows of I], B = X[rows of J]
 //   warp 1            TMEM allocator; then MMA issuer (one lane, leader CTA)
-//   warps 2 .. 2+E-1  epilogue (E = 8 or 16): tcgen05.ld -> counts -> MI -> global
-//   warp 2+E          pacer (leader CTA, when pacing is on): publishes this
-//                     pair's k-block progress and the minimum over all pairs
+//   warps 2 .. 2+E-1  epilogue (E = 8): tcgen05.ld -> counts -> MI -> global
+//   warp 2+E          pacer (leader CTA, PACE builds): publishes this pair's
+//                     k-block progress and the minimum over all pairs
 // CG == 2: a CTA pair (cluster of 2) computes a 256x256 tile with
 // tcgen05.mma.cta_group::2 (M=256, N=256); each CTA stages half of A and half
-// of B, and owns 128 accumulator rows.  CG == 1: 128x128 tiles on one SM.
+// of B, and owns 128 accumulator rows.  CG == 1: 128x128 tiles on one SM
+// (int8 only).  TMEM: int8 -- two accumulators (double-buffered); e2m1 -- one
+// accumulator, a spare copy region and the block scales (see kSfCol below).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -49,7 +52,7 @@ struct Cfg {
     static constexpr int MMA_M = 128 * CG;
     static constexpr int MMA_N = 128 * CG;
     static constexpr int ACC_COLS = MMA_N;          // TMEM columns per accumulator
-    static constexpr int TMEM_COLS = 2 * ACC_COLS;  // double-buffered
+    static constexpr int TMEM_COLS = 2 * ACC_COLS;  // int8: two accumulators; e2m1: one + spare + scales
     static constexpr int EPI_WARPS = EW;
     static constexpr int PACER_WARP = kEpiWarp0 + EW;
     static constexpr int THREADS = 32 * (kEpiWarp0 + EW);   // + one pacer warp when pacing
