@@ -40,6 +40,10 @@ extern "C" {
 #define MI_ERR_UNSUPPORTED 5 /* not an sm_100 device, or no device   */
 #define MI_ERR_FORMAT 6      /* FormatError (a malformed BMI1 file)  */
 
+/* ld_out value selecting the packed upper-triangle output: element (i, j >= i)
+ * at i*m - i*(i-1)/2 + (j - i), m(m+1)/2 elements, nothing mirrored. */
+#define MI_PACKED_UPPER 0
+
 /* engine modes (engine.py:28, EngineConfig.mode) */
 #define MI_MODE_EXACT 0
 #define MI_MODE_EPSILON 1
@@ -100,7 +104,8 @@ int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_c
                             int64_t ld, void* d_colstat, int32_t* d_colsum, const uint8_t* d_block_mask,
                             void* stream);
 /* Fused G11 + MI over the listed upper-triangle tiles; writes each tile and
- * its mirror into d_out (row-major, pitch ld_out elements). */
+ * its mirror into d_out (row-major, pitch ld_out elements), or with ld_out =
+ * MI_PACKED_UPPER only the elements j >= i, packed (see above). */
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
                int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
                int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
@@ -117,6 +122,10 @@ int mi_generate_words(uint64_t* d_words, int64_t n_rows, int64_t n_cols, uint64_
  * or float32 (MI_OUT_F32). */
 int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,
                       double epsilon, int include_diagonal, int out_kind, void* h_out, int device);
+/* the same result as the packed upper triangle (MI_PACKED_UPPER layout,
+ * n_cols (n_cols+1)/2 elements in h_out): half the device-to-host bytes */
+int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,
+                             double epsilon, int include_diagonal, int out_kind, void* h_out, int device);
 /* _kernels.gram_ones_kernel(words, out): words is n_cols x n_words; out is
  * n_cols x n_cols int64 (both triangles, diagonal = column sums). */
 int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, int64_t* h_out,

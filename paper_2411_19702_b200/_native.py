@@ -33,6 +33,7 @@ MI_MODE_EPSILON = 1
 MI_OUT_COUNTS = 0
 MI_OUT_F64 = 1
 MI_OUT_F32 = 2
+MI_PACKED_UPPER = 0  # ld_out selecting the packed upper-triangle output
 
 _ERRORS = {
     MI_ERR_DIMENSION: DimensionError,
@@ -66,6 +67,7 @@ SIGNATURES = {
     "mi_gram_mi": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
     "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
+    "mi_all_pairs_host_packed": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
     "mi_gram_ones_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_column_sums_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_bmi_header": (_int, [ctypes.c_char_p, _vp, _vp]),

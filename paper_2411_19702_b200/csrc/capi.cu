@@ -558,7 +558,8 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     if (ld < mi_kmajor_ld(n_rows) || ld % 128)
         return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
                     (long long)mi_kmajor_ld(n_rows));
-    if (ld_out < n_cols) return fail(MI_ERR_DIMENSION, "ld_out %lld < n_cols", (long long)ld_out);
+    if (ld_out != MI_PACKED_UPPER && ld_out < n_cols)
+        return fail(MI_ERR_DIMENSION, "ld_out %lld < n_cols (or MI_PACKED_UPPER)", (long long)ld_out);
     if (n_tiles < 0 || n_tiles > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "bad n_tiles");
     if (n_tiles == 0) return MI_OK;
     if (out_kind == MI_OUT_COUNTS && mode != MI_MODE_EXACT)
@@ -635,8 +636,23 @@ int mi_generate_words(uint64_t* d_words, int64_t n_rows, int64_t n_cols, uint64_
     return MI_OK;
 }
 
+int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                        int include_diagonal, int out_kind, void* h_out, int device, bool packed);
+
 int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
                       int include_diagonal, int out_kind, void* h_out, int device) {
+    return all_pairs_host_impl(h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out, device,
+                               false);
+}
+
+int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                             int include_diagonal, int out_kind, void* h_out, int device) {
+    return all_pairs_host_impl(h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out, device,
+                               true);
+}
+
+int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                        int include_diagonal, int out_kind, void* h_out, int device, bool packed) {
     int rc = check_shape(n_rows, n_cols);
     if (rc) return rc;
     if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
@@ -658,7 +674,11 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     stamp("H2D + unpack enqueued");
     const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
     const size_t row_bytes = (size_t)n_cols * esz;
-    if ((rc = ensure(&ws->out, &ws->out_cap, row_bytes * (size_t)n_cols))) return rc;
+    // byte offset of row r's first element in the output (full or packed upper triangle)
+    auto row_off = [&](int64_t r) -> size_t {
+        return packed ? (size_t)(r * n_cols - (r * (r - 1)) / 2) * esz : (size_t)r * row_bytes;
+    };
+    if ((rc = ensure(&ws->out, &ws->out_cap, row_off(n_cols)))) return rc;
     // per-tile-row completion counters in pinned, mapped host memory
     const int tile = mi_tile_size();
     const int64_t T = tiles_per_side(n_cols);
@@ -684,8 +704,8 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
         const TailPlan tp = tail_plan(nt, (int)cg, info.num_sms / (int)cg, (int)(mi_kmajor_ld(n_rows) / 128));
         for (int64_t k = 0; k < nt; ++k) expect[(size_t)tl[2 * k]] += cg * (k >= tp.n_full ? (unsigned)tp.epi : 1u);
     }
-    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out, n_cols,
-                        info, ws->row_done_d)))
+    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out,
+                        packed ? MI_PACKED_UPPER : n_cols, info, ws->row_done_d)))
         return rc;
     stamp("fused kernel enqueued");
     // Stream finished rows to the host while the GEMM continues: rows of tile
@@ -695,7 +715,7 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
     // accumulate, so chunks grow (a handful of copies in all; each extra copy
     // costs ~25 us of engine time, tools/d2h_streams.py), yet the queued one
     // keeps the copy engine from idling between them.
-    const int64_t min_chunk_rows = (int64_t)((16u << 20) / row_bytes) + 1;
+    const int64_t min_chunk_rows = (int64_t)((16u << 20) / row_bytes) + 1;  // (packed: rows shrink; fine)
     int64_t copied = 0, I = 0;
     bool kernel_done = false;
     if (!ws->copy_ev[0]) {
@@ -715,8 +735,8 @@ int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, i
         if (kernel_done) final_rows = n_cols;
         if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols) &&
             (kernel_done || in_flight() < 2)) {
-            MI_CUDA(cudaMemcpyAsync((char*)h_out + copied * row_bytes, (char*)ws->out + copied * row_bytes,
-                                    (size_t)(final_rows - copied) * row_bytes, cudaMemcpyDeviceToHost, ws->copy_stream));
+            MI_CUDA(cudaMemcpyAsync((char*)h_out + row_off(copied), (char*)ws->out + row_off(copied),
+                                    row_off(final_rows) - row_off(copied), cudaMemcpyDeviceToHost, ws->copy_stream));
             MI_CUDA(cudaEventRecord(ws->copy_ev[issued & 1], ws->copy_stream));
             ++issued;
             if (verbose) {

@@ -310,6 +310,15 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
         return;
     }
     if (!row_ok) return;
+    if (ld == 0) {
+        // packed upper triangle (ld_out = 0): element (i, j >= i) at
+        // i m - i (i - 1) / 2 + (j - i); no mirror, nothing below the diagonal
+        T* row = out + ((int64_t)i * m - ((int64_t)i * (i - 1)) / 2 - i);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (j0 + k < m && j0 + k >= i) row[j0 + k] = v[k];
+        return;
+    }
     // 2) mirror tile: row j, column i (coalesced across the warp)
     const bool hint = (p.debug & 8) != 0;
     const uint64_t pol = hint ? l2_policy_evict_first() : 0ull;

@@ -173,9 +173,12 @@ class MIEngine:
         return Prepared(n_rows, n_cols, ld, m_pad, x, colsum, colstat)
 
     def compute(self, prep: Prepared, cfg=None, out_dtype: torch.dtype = torch.float64,
-                tiles: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+                tiles: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                packed: bool = False) -> torch.Tensor:
         """Kernels 2+3: fused Gram + MI over `tiles` (all upper-triangle tiles by
-        default), each written with its mirror into `out` (m x m)."""
+        default), each written with its mirror into `out` (m x m) -- or, with
+        ``packed``, only j >= i into a flat m(m+1)/2 tensor (row-major upper
+        triangle; ``unpack_upper`` restores the square)."""
         if out_dtype not in _OUT_KIND:
             raise DomainError(f"out_dtype must be float64, float32 or int32, got {out_dtype}")
         mode, eps, diag = _config_fields(cfg)
@@ -183,15 +186,24 @@ class MIEngine:
         if kind == nat.MI_OUT_COUNTS:
             mode = nat.MI_MODE_EXACT
         m = prep.n_cols
-        if out is None:
-            out = torch.empty((m, m), dtype=out_dtype, device=self.device)
-        if out.dtype != out_dtype or out.dim() != 2 or out.shape[0] < m or out.shape[1] < m \
-                or out.stride(1) != 1 or out.device != self.device:
-            raise DimensionError("out must be a row-major (>= m, >= m) tensor of out_dtype on the device")
+        if packed:
+            if out is None:
+                out = torch.empty((m * (m + 1) // 2,), dtype=out_dtype, device=self.device)
+            if out.dtype != out_dtype or out.dim() != 1 or out.numel() < m * (m + 1) // 2 or out.stride(0) != 1 \
+                    or out.device != self.device:
+                raise DimensionError("packed out must be a flat m(m+1)/2 tensor of out_dtype on the device")
+            ld_out = nat.MI_PACKED_UPPER
+        else:
+            if out is None:
+                out = torch.empty((m, m), dtype=out_dtype, device=self.device)
+            if out.dtype != out_dtype or out.dim() != 2 or out.shape[0] < m or out.shape[1] < m \
+                    or out.stride(1) != 1 or out.device != self.device:
+                raise DimensionError("out must be a row-major (>= m, >= m) tensor of out_dtype on the device")
+            ld_out = out.stride(0)
         if tiles is None:
             tiles = self.tiles(m)
         nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m, prep.ld,
-                                       mode, eps, diag, kind, out.data_ptr(), out.stride(0),
+                                       mode, eps, diag, kind, out.data_ptr(), ld_out,
                                        tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),
                   "mi_gram_mi")
         return out
@@ -216,10 +228,13 @@ class MIEngine:
         return g, prep.colsum[:n_cols]
 
     def all_pairs_host(self, words: np.ndarray | torch.Tensor, n_rows: int, n_cols: int, cfg=None,
-                       out_dtype: torch.dtype = torch.float64, host_out: torch.Tensor | None = None) -> torch.Tensor:
+                       out_dtype: torch.dtype = torch.float64, host_out: torch.Tensor | None = None,
+                       packed: bool = False) -> torch.Tensor:
         """Host words in, host MI out, through the C ABI's mi_all_pairs_host:
         H2D, kernel 1, the fused kernel, and a D2H of finished row bands that
-        overlaps the GEMM.  ``host_out`` should be pinned for full PCIe speed."""
+        overlaps the GEMM.  ``host_out`` should be pinned for full PCIe speed.
+        ``packed``: the upper triangle only (mi_all_pairs_host_packed), a flat
+        m(m+1)/2 tensor -- half the device-to-host bytes."""
         mode, eps, diag = _config_fields(cfg)
         if out_dtype not in (torch.float64, torch.float32):
             raise DomainError(f"out_dtype must be float64 or float32, got {out_dtype}")
@@ -234,14 +249,16 @@ class MIEngine:
             if keep.dtype != np.uint64 or keep.shape != (n_cols, n_words(n_rows)):
                 raise DimensionError(f"words must be uint64 with shape {(n_cols, n_words(n_rows))}")
             wptr = keep.ctypes.data
+        shape = (n_cols * (n_cols + 1) // 2,) if packed else (n_cols, n_cols)
         if host_out is None:
-            host_out = torch.empty((n_cols, n_cols), dtype=out_dtype, pin_memory=True)
-        if host_out.dtype != out_dtype or tuple(host_out.shape) != (n_cols, n_cols) or not host_out.is_contiguous() \
+            host_out = torch.empty(shape, dtype=out_dtype, pin_memory=True)
+        if host_out.dtype != out_dtype or tuple(host_out.shape) != shape or not host_out.is_contiguous() \
                 or host_out.device.type != "cpu":
-            raise DimensionError("host_out must be a contiguous (m, m) CPU tensor of out_dtype")
+            raise DimensionError(f"host_out must be a contiguous {shape} CPU tensor of out_dtype")
         kind = nat.MI_OUT_F64 if out_dtype == torch.float64 else nat.MI_OUT_F32
-        nat.check(nat.lib().mi_all_pairs_host(wptr, n_rows, n_cols, mode, eps, diag, kind, host_out.data_ptr(),
-                                              self.device.index), "mi_all_pairs_host")
+        fn = nat.lib().mi_all_pairs_host_packed if packed else nat.lib().mi_all_pairs_host
+        nat.check(fn(wptr, n_rows, n_cols, mode, eps, diag, kind, host_out.data_ptr(), self.device.index),
+                  "mi_all_pairs_host")
         del keep
         return host_out
 
@@ -261,6 +278,23 @@ def mi_all_pairs(data, cfg: EngineConfig | None = None, backend: str = "dense", 
     eng = MIEngine.get(device)
     host = eng.all_pairs_host(words, n, m, cfg, torch.float64)
     return MIMatrix(values=host.numpy())
+
+
+def unpack_upper(packed, m: int):
+    """Square symmetric (m, m) matrix from the packed upper triangle
+    (MI_PACKED_UPPER layout: row i holds columns i..m-1).  numpy or torch."""
+    iu = np.triu_indices(m)
+    if isinstance(packed, torch.Tensor):
+        out = torch.empty((m, m), dtype=packed.dtype, device=packed.device)
+        r = torch.from_numpy(iu[0]).to(packed.device)
+        c = torch.from_numpy(iu[1]).to(packed.device)
+        out[r, c] = packed
+        out[c, r] = packed
+        return out
+    out = np.empty((m, m), dtype=packed.dtype)
+    out[iu] = packed
+    out.T[iu] = packed
+    return out
 
 
 def gram_ones(data, device: int | None = None) -> np.ndarray:

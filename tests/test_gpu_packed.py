@@ -1,0 +1,33 @@
+"""Egress: the packed upper-triangle output (MI_PACKED_UPPER:
+row i holds columns i..m-1, m(m+1)/2 elements) through the device API and the
+streamed host API is exactly the upper triangle of the full result."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rand_bits
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (100, 7), (777, 300), (4_097, 1_300), (5_000, 3_000), (20_000, 700)])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_packed_equals_upper_triangle(engine, n, m, dtype):
+    from paper_2411_19702_b200.engine import unpack_upper
+
+    rng = np.random.default_rng(n * 3 + m)
+    words = O.pack_bits(rand_bits(rng, n, m, 0.4))
+    dt = getattr(torch, dtype)
+    dev = engine.upload(words)
+    full = engine.all_pairs_device(dev, n, m, None, dt).cpu().numpy()
+    prep = engine.prepare(dev, n, m)
+    packed = engine.compute(prep, None, dt, packed=True).cpu().numpy()
+    iu = np.triu_indices(m)
+    assert np.array_equal(packed, full[iu])
+    assert np.array_equal(unpack_upper(packed, m), full)
+    host = engine.all_pairs_host(words, n, m, None, dt, packed=True).numpy()
+    assert np.array_equal(host, full[iu])
