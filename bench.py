@@ -420,6 +420,7 @@ def nat_num_tiles(m: int) -> int:
 
 
 def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -430,20 +431,29 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
     esz = 8 if out_dtype == torch.float64 else 4
     words_bytes = m * ((n + 63) // 64) * 8
     host_words = words_dev.cpu().pin_memory() if rank == 0 else None
-    host_out = torch.empty((m, m), dtype=out_dtype, pin_memory=True) if rank == 0 else None
+    host_out = torch.empty((m, m), dtype=out_dtype, pin_memory=True) if (rank == 0 and world == 1) else None
     steps = max(1, min(args.steps, 20))
     shard_buf = torch.empty((m, m), dtype=out_dtype, device=dev) if world > 1 else None
+    shared = None
+    if world > 1:
+        # one host matrix in node shared memory; every rank writes its share of
+        # it over its own PCIe link (dispatch.mi_all_pairs_to_host)
+        from paper_2411_19702_b200.hostshm import SharedHostMatrix
+
+        name = f"mi_b200_bench_{os.environ.get('MASTER_PORT', '0')}"
+        np_dt = np.float64 if out_dtype == torch.float64 else np.float32
+        if rank == 0:
+            shared = SharedHostMatrix(name, m, np_dt, create=True)
+        dist.barrier()
+        if rank != 0:
+            shared = SharedHostMatrix(name, m, np_dt, create=False)
 
     def once():
         if world == 1:
             eng.all_pairs_host(host_words, n, m, cfg, out_dtype, host_out=host_out)
         else:
             w = host_words.to(dev, non_blocking=True) if rank == 0 else None
-            local, _ = dsp.mi_all_pairs_sharded(eng, w, n, m, cfg, out_dtype, out=shard_buf, zero_fill=True)
-            full = dsp.gather_to_root(local, m)
-            if rank == 0:
-                host_out.copy_(full, non_blocking=True)
-            stream.synchronize()
+            dsp.mi_all_pairs_to_host(eng, w, n, m, shared, cfg, out_dtype, out=shard_buf)
 
     for _ in range(2):
         once()
@@ -462,6 +472,9 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    if shared is not None:
+        dist.barrier()
+        shared.close()
     packed = None
     if world == 1:  # egress variant: the packed upper triangle (half the D2H), informational
         pk_out = torch.empty((m * (m + 1) // 2,), dtype=out_dtype, pin_memory=True)
@@ -482,7 +495,8 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
     return {"value": W / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": words_bytes,
             "d2h_bytes_per_step": m * m * esz, "ms_per_step": ms, "steps": steps, "packed_upper": packed,
             "api": "MIEngine.all_pairs_host (pinned words in, pinned MI out)" if world == 1 else
-                   "dispatch.mi_all_pairs_sharded + gather_to_root"}
+                   "dispatch.mi_all_pairs_to_host (words H2D on rank 0, broadcast, sharded compute, every rank "
+                   "copies its share into one shared-memory host matrix)"}
 
 
 def operand_is_fp4(n_rows: int) -> bool:

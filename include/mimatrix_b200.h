@@ -133,6 +133,19 @@ int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, 
 /* binmat.column_sums(matrix) */
 int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, uint64_t* h_out,
                         int device);
+/* ---- egress of a sharded result into one host matrix ----
+ * Pin host memory allocated elsewhere (e.g. a POSIX shared-memory segment
+ * that every rank on the node maps) for asynchronous copies. */
+int mi_host_register(void* h_ptr, int64_t bytes);
+int mi_host_unregister(void* h_ptr);
+/* Copy the listed tiles (h_tiles: host (I, J) pairs as from mi_tile_list) and
+ * their mirrors from d_out (pitch ld_out elements of esz = 4 or 8 bytes) into
+ * h_dst (pitch ld_dst), clipped to n_cols, as merged 2-D copies on `stream`
+ * (asynchronous): every rank writes its share of the full matrix over its own
+ * PCIe link. */
+int mi_copy_tiles_to_host(const void* d_out, int64_t ld_out, int64_t n_cols, int esz, const int32_t* h_tiles,
+                          int64_t n_tiles, void* h_dst, int64_t ld_dst, void* stream);
+
 /* ---- ingest: the BMI1 packed container (io.py:1-16, read_bmi io.py:92-116) ----
  * "BMI1", n_rows (u64 LE), n_cols (u64 LE), then n_cols columns of
  * ceil(n_rows/64) little-endian words -- byte for byte the words layout, so

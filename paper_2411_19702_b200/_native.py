@@ -70,6 +70,9 @@ SIGNATURES = {
     "mi_all_pairs_host_packed": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
     "mi_gram_ones_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_column_sums_host": (_int, [_vp, _i64, _i64, _vp, _int]),
+    "mi_host_register": (_int, [_vp, _i64]),
+    "mi_host_unregister": (_int, [_vp]),
+    "mi_copy_tiles_to_host": (_int, [_vp, _i64, _i64, _int, _vp, _i64, _vp, _i64, _vp]),
     "mi_bmi_header": (_int, [ctypes.c_char_p, _vp, _vp]),
     "mi_bmi_load": (_int, [ctypes.c_char_p, _vp, _i64, _i64, _vp]),
     "mi_set_tuning": (_int, [ctypes.c_char_p, _int]),

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <chrono>
 #include <mutex>
 #include <thread>
@@ -798,6 +799,72 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
     MI_CUDA(cudaMemcpyAsync(tmp.data(), ws->colsum, (size_t)n_cols * 4, cudaMemcpyDeviceToHost, ws->stream));
     MI_CUDA(cudaStreamSynchronize(ws->stream));
     for (int64_t k = 0; k < n_cols; ++k) h_out[k] = (uint64_t)tmp[k];
+    return MI_OK;
+}
+
+// ---------------------------------------------------------------- sharded egress
+
+int mi_host_register(void* h_ptr, int64_t bytes) {
+    if (!h_ptr || bytes < 1) return fail(MI_ERR_DOMAIN, "bad host range");
+    MI_CUDA(cudaHostRegister(h_ptr, (size_t)bytes, cudaHostRegisterPortable));
+    return MI_OK;
+}
+
+int mi_host_unregister(void* h_ptr) {
+    if (!h_ptr) return fail(MI_ERR_DOMAIN, "null host pointer");
+    MI_CUDA(cudaHostUnregister(h_ptr));
+    return MI_OK;
+}
+
+// Tiles and their mirrors, device -> host, as few 2-D copies as possible: runs
+// of consecutive J in a tile row merge, then identical runs in consecutive tile
+// rows (an 8-rank column-group share is one or two rectangles).
+int mi_copy_tiles_to_host(const void* d_out, int64_t ld_out, int64_t n_cols, int esz, const int32_t* h_tiles,
+                          int64_t n_tiles, void* h_dst, int64_t ld_dst, void* stream) {
+    if (!d_out || !h_dst || (n_tiles > 0 && !h_tiles)) return fail(MI_ERR_DOMAIN, "null argument");
+    if (esz != 4 && esz != 8) return fail(MI_ERR_DOMAIN, "esz must be 4 or 8");
+    if (ld_out < n_cols || ld_dst < n_cols) return fail(MI_ERR_DIMENSION, "pitch < n_cols");
+    const int64_t t = mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
+    std::vector<std::pair<int32_t, int32_t>> v;
+    v.reserve((size_t)n_tiles);
+    for (int64_t k = 0; k < n_tiles; ++k) {
+        const int32_t I = h_tiles[2 * k], J = h_tiles[2 * k + 1];
+        if (I < 0 || J < 0 || I >= T || J >= T) return fail(MI_ERR_DIMENSION, "tile (%d, %d) outside %lld", I, J, (long long)T);
+        v.push_back({I, J});
+    }
+    std::sort(v.begin(), v.end());
+    struct Run { int32_t I, J0, J1; };  // tile row I, tile columns [J0, J1)
+    std::vector<Run> runs;
+    for (size_t k = 0; k < v.size();) {
+        size_t e = k + 1;
+        while (e < v.size() && v[e].first == v[k].first && v[e].second == v[e - 1].second + 1) ++e;
+        runs.push_back({v[k].first, v[k].second, v[e - 1].second + 1});
+        k = e;
+    }
+    struct Rect { int32_t I0, I1, J0, J1; };
+    std::vector<Rect> rects;
+    for (const Run& r : runs) {
+        if (!rects.empty() && rects.back().I1 == r.I && rects.back().J0 == r.J0 && rects.back().J1 == r.J1)
+            rects.back().I1 = r.I + 1;
+        else
+            rects.push_back({r.I, r.I + 1, r.J0, r.J1});
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    auto copy = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+        r1 = r1 < n_cols ? r1 : n_cols;
+        c1 = c1 < n_cols ? c1 : n_cols;
+        if (r0 >= r1 || c0 >= c1) return MI_OK;
+        MI_CUDA(cudaMemcpy2DAsync((char*)h_dst + (r0 * ld_dst + c0) * esz, (size_t)(ld_dst * esz),
+                                  (const char*)d_out + (r0 * ld_out + c0) * esz, (size_t)(ld_out * esz),
+                                  (size_t)((c1 - c0) * esz), (size_t)(r1 - r0), cudaMemcpyDeviceToHost, st));
+        return MI_OK;
+    };
+    int rc;
+    for (const Rect& q : rects) {
+        if ((rc = copy(q.I0 * t, q.I1 * t, q.J0 * t, q.J1 * t))) return rc;  // tiles
+        if ((rc = copy(q.J0 * t, q.J1 * t, q.I0 * t, q.I1 * t))) return rc;  // mirrors
+    }
     return MI_OK;
 }
 

@@ -119,3 +119,28 @@ def mi_all_pairs_sharded(engine, words: torch.Tensor | None, n_rows: int, n_cols
 
     tiles = run_sharded(words, n_rows, n_cols, compute, out, engine.device, group)
     return out, tiles
+
+
+def copy_share_to_host(engine, local: torch.Tensor, n_cols: int, tiles: np.ndarray, host) -> None:
+    """This rank's tiles and mirrors, device -> the shared host matrix
+    (hostshm.SharedHostMatrix), as merged 2-D copies; returns once copied."""
+    t = np.ascontiguousarray(np.asarray(tiles, dtype=np.int32))
+    stream = torch.cuda.current_stream(engine.device)
+    nat.check(nat.lib().mi_copy_tiles_to_host(local.data_ptr(), local.stride(0), n_cols, local.element_size(),
+                                              t.ctypes.data, t.shape[0], host.ptr, n_cols, stream.cuda_stream),
+              "mi_copy_tiles_to_host")
+    stream.synchronize()
+
+
+def mi_all_pairs_to_host(engine, words: torch.Tensor | None, n_rows: int, n_cols: int, host, cfg=None,
+                         out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
+                         group=None) -> np.ndarray:
+    """Sharded compute, then every rank writes its share into the shared host
+    matrix over its own PCIe link; after the barrier the full matrix is in
+    ``host.array`` on every rank of the node."""
+    local, tiles = mi_all_pairs_sharded(engine, words, n_rows, n_cols, cfg, out_dtype, out=out, group=group)
+    copy_share_to_host(engine, local, n_cols, tiles, host)
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier(group=group)
+    return host.array
+

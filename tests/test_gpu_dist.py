@@ -111,3 +111,61 @@ def test_eight_rank_shares_in_one_process(engine, n, m, dtype):
         engine.compute(prep, None, dt, tiles=engine.tiles(m, r, 8), out=out)
         acc += out
     assert torch.equal(acc, full)
+
+
+def _host_worker(rank, world, port, n, m, name, result_q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    host = None
+    try:
+        from paper_2411_19702_b200 import datagen, dispatch
+        from paper_2411_19702_b200.engine import MIEngine
+        from paper_2411_19702_b200.hostshm import SharedHostMatrix
+
+        torch.cuda.set_device(0)
+        eng = MIEngine.get(0)
+        if rank == 0:
+            host = SharedHostMatrix(name, m, np.float64, create=True)
+        dist.barrier()
+        if rank != 0:
+            host = SharedHostMatrix(name, m, np.float64, create=False)
+        words = datagen.generate_words_device(datagen.config_recipe(2, n, m), eng.device) if rank == 0 else None
+        full = dispatch.mi_all_pairs_to_host(eng, words, n, m, host)
+        if rank == 0:
+            ref = eng.all_pairs_device(words, n, m).cpu().numpy()
+            result_q.put(("ok", bool(np.array_equal(full, ref)), 0))
+        else:
+            result_q.put(("peer", True, 0))
+        dist.barrier()
+    except Exception as exc:  # pragma: no cover
+        import traceback
+        result_q.put(("error", repr(exc) + traceback.format_exc(), 0))
+    finally:
+        if host is not None:
+            host.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_write_one_shared_host_matrix(world):
+    """Every rank copies its tiles and mirrors into one POSIX shared-memory
+    host matrix (mi_host_register + mi_copy_tiles_to_host); the assembled
+    matrix equals the single-process result."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    name = f"mi_b200_test_{os.getpid()}_{world}"
+    procs = [ctx.Process(target=_host_worker, args=(r, world, port, 5_000, 1_300, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    errors = [r for r in results if r[0] == "error"]
+    assert not errors, errors
+    assert [r for r in results if r[0] == "ok"][0][1]
