@@ -505,7 +505,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     const uint32_t tmem_base = *tmem_slot_ptr;
     constexpr int NACC = FP4 ? 1 : 2;  // accumulator buffers
     if constexpr (FP4) {
-        // block scales = 1.0 everywhere in TMEM columns [256, 512) of both CTAs
+        // block scales = 1.0 (E8M0 127) in TMEM columns [kSfCol, kSfCol + 16) of both CTAs
         if (etid >= 0 && etid < 4 * 32) {  // one warp per TMEM lane quadrant
             const uint32_t one[16] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
                                       0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
