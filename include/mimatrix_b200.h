@@ -165,14 +165,16 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per
  * band of the tile order), "stages" (smem ring depth), "epi_warps" (8 or 16
  * epilogue warps), "fixed" (exact-mode epilogue: 1 adaptive per tile, default;
- * 0 FP64 only; 2 fixed-point table only), "table_thr" (adaptive threshold on
+ * 0 FP64 only; 2 fixed-point table only; 3 hybrid only), "table_thr" (adaptive threshold on
  * the tile's column-sum spread), "pace" (L2 pacing window in k-blocks that
  * keeps the SM pairs' K sweeps together: -1 auto (default), 0 off), "tail"
  * (the last partial round of tiles split over the idle SM pairs: 1 auto,
  * default; 0 off; 2 column slices; 3 K ranges), "fp4" (1 = e2m1 operands on
  * kind::mxf4 when N < 2^24, default; 0 = int8), "evac" (e2m1: evacuate the
  * accumulator before FP64-free epilogues; 1 default, 0 off, 2 always),
- * "shard" (8 ranks: 1 = column-group pairs, default; 0 = round robin).  Also
+ * "shard" (8 ranks: 1 = column-group pairs, default; 0 = round robin),
+ * "hybrid" (exact-mode tiles off the table path: 0 = FP64, default; 1 = three
+ * table gathers + T(c00) computed -- slower on every config measured).  Also
  * settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */

@@ -57,7 +57,8 @@ int env_int(const char* name, int dflt) {
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
-    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard;
+    int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
+        hybrid;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -65,7 +66,8 @@ Tuning& tuning() {
                        env_int("MI_B200_STAGES", 6), env_int("MI_B200_EPI_WARPS", 8), env_int("MI_B200_DEBUG", 0),
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
-                       env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1)};
+                       env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
+                       env_int("MI_B200_HYBRID", 0)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -258,6 +260,13 @@ int2* blkrange_ptr(void* colstat, int64_t n_rows, int64_t n_cols) {
     return t ? reinterpret_cast<int2*>(t + n_rows + 1) : nullptr;
 }
 
+// fix_xlog2x's mantissa tables (kFixR, kFixLG) in global memory, after the
+// block ranges: the hybrid epilogue evaluates T(c00) with them through L1.
+float* fixr_ptr(void* colstat, int64_t n_rows, int64_t n_cols) {
+    int2* b = blkrange_ptr(colstat, n_rows, n_cols);
+    return b ? reinterpret_cast<float*>(b + mi_kmajor_rows(n_cols) / 128) : nullptr;
+}
+
 // rcp = round(2^(62 + nb) / N) and off0 = -(nb - 2) - s for fixed_to_fp
 void fixed_point_consts(int64_t N, unsigned long long* rcp, int* off0) {
     int nb = 0;
@@ -415,7 +424,8 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
     MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
                                  (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
-                                 blkrange_ptr(ws.colstat, n_rows, n_cols), operand_fp4(n_rows), nullptr,
+                                 blkrange_ptr(ws.colstat, n_rows, n_cols), fixr_ptr(ws.colstat, n_rows, n_cols),
+                                 operand_fp4(n_rows), nullptr,
                                  mi_tile_size(), info.num_sms, ws.stream));
     *ld_out = ld;
     *m_pad_out = m_pad;
@@ -477,7 +487,9 @@ int64_t mi_kmajor_rows(int64_t n_cols) { return round_up(n_cols < 1 ? 1 : n_cols
 
 int64_t mi_colstat_bytes(int64_t n_rows, int64_t n_cols) {
     const int64_t stats = mi_kmajor_rows(n_cols) * (int64_t)sizeof(ColStat);
-    const int64_t table = (n_rows >= 1 && n_rows < kXlogxMaxN) ? (n_rows + 1) * 8 + mi_kmajor_rows(n_cols) / 128 * 8 : 0;
+    const int64_t table = (n_rows >= 1 && n_rows < kXlogxMaxN)
+                              ? (n_rows + 1) * 8 + mi_kmajor_rows(n_cols) / 128 * 8 + kFixTabBytes
+                              : 0;
     return stats + table;
 }
 
@@ -536,7 +548,8 @@ int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_c
     if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
     MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
                                  (ColStat*)d_colstat, xlogx_ptr(d_colstat, n_rows, n_cols),
-                                 blkrange_ptr(d_colstat, n_rows, n_cols), operand_fp4(n_rows), d_block_mask,
+                                 blkrange_ptr(d_colstat, n_rows, n_cols), fixr_ptr(d_colstat, n_rows, n_cols),
+                                 operand_fp4(n_rows), d_block_mask,
                                  mi_tile_size(), info.num_sms, (cudaStream_t)stream));
     return MI_OK;
 }
@@ -614,8 +627,12 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.fix_s = xlogx_scale(n_rows);
     p.xlogx = xlogx_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
     p.blkrange = blkrange_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+    p.fix_r = fixr_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+    p.fix_lg = p.fix_r ? reinterpret_cast<const float2*>(p.fix_r + (1 << kFixLogBitsH)) : nullptr;
     // exact-mode epilogue: 0 = FP64 only, 1 = adaptive per tile (default), 2 = table only
-    p.table_thr = tuning().fixed == 0 ? -1 : tuning().fixed == 2 ? 0x7FFFFFFF : tuning().table_thr;
+    p.table_thr = tuning().fixed == 0 ? -1 : tuning().fixed == 2 ? 0x7FFFFFFF : tuning().fixed == 3 ? -1 : tuning().table_thr;
+    // tiles that miss the table threshold: hybrid (fixed 1 with hybrid on, or 3) or FP64
+    p.hybrid = (tuning().fixed == 3 || (tuning().fixed == 1 && tuning().hybrid)) && p.fix_r ? 1 : 0;
     int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
     MI_CUDA(launch_gram_mi(cta_group(), operand_fp4(n_rows), out_kind, eff_mode, tuning().stages, tuning().epi_warps,
@@ -973,11 +990,14 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "table_thr")) {
         t.table_thr = value;
     } else if (!strcmp(key, "fixed")) {
-        if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "fixed must be 0, 1 or 2");
+        if (value < 0 || value > 3) return fail(MI_ERR_DOMAIN, "fixed must be 0, 1, 2 or 3");
         t.fixed = value;
     } else if (!strcmp(key, "tail")) {
         if (value < 0 || value > 3) return fail(MI_ERR_DOMAIN, "tail must be 0 (off), 1 (auto), 2 (slices) or 3 (K ranges)");
         t.tail = value;
+    } else if (!strcmp(key, "hybrid")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "hybrid must be 0 or 1");
+        t.hybrid = value;
     } else if (!strcmp(key, "shard")) {
         if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "shard must be 0 (round robin) or 1 (column groups)");
         t.shard = value;
@@ -1015,6 +1035,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "fp4")) return t.fp4;
     if (!strcmp(key, "evac")) return t.evac;
     if (!strcmp(key, "shard")) return t.shard;
+    if (!strcmp(key, "hybrid")) return t.hybrid;
     return -1;
 }
 

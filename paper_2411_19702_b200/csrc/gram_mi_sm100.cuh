@@ -257,7 +257,12 @@ struct RowQ {
 // FP64 -- B200 runs FP64 on the tensor datapath, ~23x slower under tcgen05.mma);
 // otherwise the FP64 epilogue (epsilon mode, and exact-mode tiles whose column
 // sums are too spread out for the table gathers to stay in L1).
-template <int OUT, int MODE, bool DIAG, bool TABLE, typename T>
+// HYB (with TABLE): the hybrid path -- T(g), T(a - g), T(b - g) gathered, T(c00)
+// evaluated by the table's own generating function fix_xlog2x (bit-identical to
+// the entry, so exactness is unchanged): c00 = N - a - b + g is the one
+// argument that scatters over the table when column sums are spread, and its
+// L1 misses are what rules the full table out for such tiles.
+template <int OUT, int MODE, bool DIAG, bool TABLE, bool HYB, typename T>
 __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A, const RowQ& AQ,
                                            const ColS* __restrict__ cols, const ColS& Arow,
                                            const GramMiParams& p, double eN, double fN, double dN, double rN,
@@ -278,8 +283,10 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
             const int g = (int)r[k];
             const int bv = cols[k].vi;
             const long long* __restrict__ X = p.xlogx;
-            const long long S = (__ldg(X + g) + __ldg(X + (AQ.v - g))) +
-                                (__ldg(X + (bv - g)) + __ldg(X + (AQ.nmv - bv + g))) + (AQ.kq - cols[k].q);
+            const long long t00 = HYB ? fix_xlog2x((unsigned)(AQ.nmv - bv + g), p.fix_s, p.fix_r, p.fix_lg)
+                                      : __ldg(X + (AQ.nmv - bv + g));
+            const long long S = (__ldg(X + g) + __ldg(X + (AQ.v - g))) + (__ldg(X + (bv - g)) + t00) +
+                                (AQ.kq - cols[k].q);
             T x = fixed_to_fp<T>(S, p.rcp, p.off0);
             if (DIAG && !p.include_diagonal && i == j) x = (T)0;
             v[k] = x;
@@ -697,7 +704,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             cpar ^= 1;
             ColS Arow{};
             RowQ AQ{0, 0, 0};
-            bool use_table = false;
+            bool use_table = false, use_hybrid = false;
             if constexpr (OUT != MI_OUT_COUNTS) {
                 if (etid < C::TS) cols[etid] = col_s(p.colstat[tile.y * C::TS + etid]);
                 named_barrier_sync(2, EW * 32);
@@ -724,6 +731,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     }
                     spread += hi >= lo ? hi - lo : 0;
                     use_table = spread <= p.table_thr;
+                    use_hybrid = !use_table && p.hybrid;
                 }
             }
             const RowMarg A = row_marg(Arow, eN, dN);
@@ -735,7 +743,8 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             // Evacuate only when the epilogue is FP64-free: an FP64 epilogue next to
             // running MMAs is throttled ~23x (r01_micro.md), so FP64-path tiles keep
             // the accumulator until done and run their epilogue alone.
-            const bool EVAC = FP4 && TAIL == 0 && p.evac != 0 && (OUT == MI_OUT_COUNTS || use_table || p.evac == 2);
+            const bool EVAC = FP4 && TAIL == 0 && p.evac != 0 &&
+                              (OUT == MI_OUT_COUNTS || use_table || use_hybrid || p.evac == 2);
             uint32_t keep[16];  // EVAC: the accumulator columns that do not fit the spare TMEM
             if (EVAC) {
 #pragma unroll 1
@@ -799,18 +808,27 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 if (use_table) {
                     if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
                         if (diag)
-                            epilogue16<OUT, MODE, true, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab,
-                                                              out, ld, row_ok, vec_ok);
+                            epilogue16<OUT, MODE, true, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
+                                                                     dN, rN, tab, out, ld, row_ok, vec_ok);
                         else
-                            epilogue16<OUT, MODE, false, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab,
-                                                               out, ld, row_ok, vec_ok);
+                            epilogue16<OUT, MODE, false, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
+                                                                      dN, rN, tab, out, ld, row_ok, vec_ok);
+                    }
+                } else if (use_hybrid) {
+                    if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
+                        if (diag)
+                            epilogue16<OUT, MODE, true, true, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
+                                                                    dN, rN, tab, out, ld, row_ok, vec_ok);
+                        else
+                            epilogue16<OUT, MODE, false, true, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
+                                                                     dN, rN, tab, out, ld, row_ok, vec_ok);
                     }
                 } else if (diag) {
-                    epilogue16<OUT, MODE, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
-                                                       row_ok, vec_ok);
+                    epilogue16<OUT, MODE, true, false, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN,
+                                                              tab, out, ld, row_ok, vec_ok);
                 } else {
-                    epilogue16<OUT, MODE, false, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN, tab, out, ld,
-                                                        row_ok, vec_ok);
+                    epilogue16<OUT, MODE, false, false, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN,
+                                                               tab, out, ld, row_ok, vec_ok);
                 }
             }
             // hand the accumulator back to the MMA warp (EVAC: done above)

@@ -38,6 +38,9 @@ struct GramMiParams {
     const long long* xlogx; // exact mode: fixed-point T(c) = c log2(c) 2^s, c = 0..N (or nullptr)
     const int2* blkrange;   // exact mode: (min, max) column sum per 128-column block
     int table_thr;          // table path when the tile's two column-sum ranges sum to <= this
+    int hybrid;             // other exact-mode tiles: 1 = hybrid (3 table gathers + T(c00) computed), 0 = FP64
+    const float* fix_r;     // fix_xlog2x mantissa tables in global memory (hybrid path)
+    const float2* fix_lg;
     unsigned int* row_done; // optional: per tile row I, +1 per CTA when its part of tile (I, J) is
                             // stored (system scope; lets the host stream finished rows to host)
     unsigned int* pace;     // optional: per-cluster k-block progress, stride kPaceStride (L2 pacing)
@@ -66,6 +69,8 @@ constexpr int kPaceStride = 8;          // u32 per cluster slot (one 32-B sector
 constexpr int kPaceMaxClusters = 256;
 constexpr int kTailMaxUnits = 148;      // split tail units (<= clusters): flag pairs and partial slots
 constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
+constexpr int kFixLogBitsH = 10;             // = kFixLogBits (fixlog_table.h), for host code
+constexpr long long kFixTabBytes = (1ll << kFixLogBitsH) * 12;  // kFixR floats + kFixLG float2s
 constexpr long long kFp4MaxN = 1ll << 24;    // e2m1 operands: fp32 accumulators exact below 2^24
 
 // fp4: operand X holds e2m1 nibbles (kind::mxf4 build, cg == 2 only), else int8 bytes
@@ -78,7 +83,7 @@ int gram_mi_tile_size(int cg);
 // band = N_pad / 2), else int8 bytes (ld = N_pad)
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
                                  int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,
-                                 ColStat* colstat, long long* xlogx, int2* blkrange, bool fp4,
+                                 ColStat* colstat, long long* xlogx, int2* blkrange, float* fixr, bool fp4,
                                  const uint8_t* block_mask, int tile, int num_sms, cudaStream_t stream);
 
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,

@@ -32,11 +32,19 @@ __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x0020
 // table path and the per-column terms agree bit for bit.
 __global__ void __launch_bounds__(256) unpack_prep_kernel(ColStat* __restrict__ colstat, int64_t m_pad,
                                                           long long* __restrict__ T, long long N, int s,
-                                                          int2* __restrict__ blkrange, int nblk) {
+                                                          int2* __restrict__ blkrange, int nblk,
+                                                          float* __restrict__ fixr) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     for (int64_t c = tid; c < m_pad; c += nthr) colstat[c].vi = 0;
     for (int64_t b = tid; b < nblk; b += nthr) blkrange[b] = make_int2(0x7FFFFFFF, -1);
+    if (fixr && blockIdx.x == 0) {  // fix_xlog2x's tables for the hybrid epilogue (read through L1)
+        float2* fixlg = reinterpret_cast<float2*>(fixr + (1 << kFixLogBits));
+        for (int q = threadIdx.x; q < (1 << kFixLogBits); q += blockDim.x) {
+            fixr[q] = kFixR[q];
+            fixlg[q] = kFixLG[q];
+        }
+    }
     if (!T) return;
     __shared__ float R[1 << kFixLogBits];
     __shared__ float2 LG[1 << kFixLogBits];
@@ -202,7 +210,8 @@ __global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m,
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
                                  int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, long long* xlogx,
-                                 int2* blkrange, bool fp4, const uint8_t* block_mask, int tile, int num_sms,
+                                 int2* blkrange, float* fixr, bool fp4, const uint8_t* block_mask, int tile,
+                                 int num_sms,
                                  cudaStream_t stream) {
     const int fix_s = xlogx_scale(n_rows);
     {
@@ -211,7 +220,8 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
         int64_t tb = (work + 255) / 256;
         if (tb > (int64_t)num_sms * 16) tb = (int64_t)num_sms * 16;
         unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, xlogx, n_rows, fix_s, blkrange,
-                                                             (xlogx && blkrange) ? (int)(m_pad / 128) : 0);
+                                                             (xlogx && blkrange) ? (int)(m_pad / 128) : 0,
+                                                             xlogx ? fixr : nullptr);
     }
     const int64_t wpad = ld / 128 * (fp4 ? 4 : 2);
     const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 KNOBS = [{}, {"tail": 2}, {"tail": 3}, {"tail": 0}, {"pace": 8}, {"fixed": 0}, {"fixed": 2},
-         {"evac": 0}, {"evac": 2}, {"fp4": 0}, {"band": 1}, {"cta_group": 1}]
+         {"evac": 0}, {"evac": 2}, {"fp4": 0}, {"band": 1}, {"cta_group": 1}, {"fixed": 3}, {"hybrid": 0}]
 
 
 def _case(k: int):
