@@ -437,23 +437,39 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
     shared = None
     if world > 1:
         # one host matrix in node shared memory; every rank writes its share of
-        # it over its own PCIe link (dispatch.mi_all_pairs_to_host)
+        # it over its own PCIe link (dispatch.mi_all_pairs_to_host) -- when
+        # /dev/shm can hold it (same answer on every rank: one node)
         from paper_2411_19702_b200.hostshm import SharedHostMatrix
 
         name = f"mi_b200_bench_{os.environ.get('MASTER_PORT', '0')}"
         np_dt = np.float64 if out_dtype == torch.float64 else np.float32
-        if rank == 0:
-            shared = SharedHostMatrix(name, m, np_dt, create=True)
-        dist.barrier()
-        if rank != 0:
-            shared = SharedHostMatrix(name, m, np_dt, create=False)
+        try:
+            st = os.statvfs("/dev/shm")
+            shm_ok = st.f_bavail * st.f_frsize > 1.2 * m * m * esz and not os.environ.get("MI_B200_NO_SHM")
+        except OSError:
+            shm_ok = False
+        if shm_ok:
+            if rank == 0:
+                shared = SharedHostMatrix(name, m, np_dt, create=True)
+            dist.barrier()
+            if rank != 0:
+                shared = SharedHostMatrix(name, m, np_dt, create=False)
+        elif rank == 0:
+            host_out = torch.empty((m, m), dtype=out_dtype, pin_memory=True)
 
     def once():
         if world == 1:
             eng.all_pairs_host(host_words, n, m, cfg, out_dtype, host_out=host_out)
-        else:
+        elif shared is not None:
             w = host_words.to(dev, non_blocking=True) if rank == 0 else None
             dsp.mi_all_pairs_to_host(eng, w, n, m, shared, cfg, out_dtype, out=shard_buf)
+        else:  # no room in /dev/shm: gather onto rank 0's GPU, one D2H
+            w = host_words.to(dev, non_blocking=True) if rank == 0 else None
+            local, _ = dsp.mi_all_pairs_sharded(eng, w, n, m, cfg, out_dtype, out=shard_buf, zero_fill=True)
+            full = dsp.gather_to_root(local, m)
+            if rank == 0:
+                host_out.copy_(full, non_blocking=True)
+            stream.synchronize()
 
     for _ in range(2):
         once()
@@ -495,8 +511,9 @@ def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W):
     return {"value": W / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": words_bytes,
             "d2h_bytes_per_step": m * m * esz, "ms_per_step": ms, "steps": steps, "packed_upper": packed,
             "api": "MIEngine.all_pairs_host (pinned words in, pinned MI out)" if world == 1 else
-                   "dispatch.mi_all_pairs_to_host (words H2D on rank 0, broadcast, sharded compute, every rank "
-                   "copies its share into one shared-memory host matrix)"}
+                   ("dispatch.mi_all_pairs_to_host (words H2D on rank 0, broadcast, sharded compute, every rank "
+                    "copies its share into one shared-memory host matrix)" if shared is not None else
+                    "dispatch.mi_all_pairs_sharded + gather_to_root + D2H on rank 0")}
 
 
 def operand_is_fp4(n_rows: int) -> bool:
