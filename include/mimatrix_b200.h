@@ -18,6 +18,13 @@
  *   mi_gram_mi          _kernels.py:48-61 + gram.py:88-111 + engine.py:93-141
  *                                           (G11, closed-form counts, MI; fused)
  *   mi_generate_words   datagen.py:44-73    generate(GenSpec) stream, packed
+ *   mi_bmi_header,      io.py:92-116        read_bmi(path) (BMI1 container, io.py:1-16),
+ *   mi_bmi_load                             payload streamed straight to the device
+ * Extensions with no reference counterpart: mi_all_pairs_host_packed and
+ * ld_out = MI_PACKED_UPPER (upper-triangle egress), mi_tile_list /
+ * mi_rank_blocks / mi_unpack_colsum_blocks (multi-GPU shares),
+ * mi_host_register / mi_copy_tiles_to_host (sharded host egress), the
+ * layout queries and the tuning knobs.
  * Error codes mirror the reference's exception classes (errors.py:8-25).
  */
 #ifndef MIMATRIX_B200_H
