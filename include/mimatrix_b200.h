@@ -23,6 +23,7 @@
  * Extensions with no reference counterpart: mi_all_pairs_host_packed and
  * ld_out = MI_PACKED_UPPER (upper-triangle egress), mi_tile_list /
  * mi_rank_blocks / mi_unpack_colsum_blocks (multi-GPU shares),
+ * mi_column_order / mi_unpack_colsum_ordered / mi_unpermute (column-sum order),
  * mi_host_register / mi_copy_tiles_to_host (sharded host egress), the
  * layout queries and the tuning knobs.
  * Error codes mirror the reference's exception classes (errors.py:8-25).
@@ -116,6 +117,25 @@ int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_c
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
                int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
                int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
+/* ---- column order by column sum (configs with spread densities) ----
+ * The fused epilogue's FP64-free table path needs each tile's column sums to
+ * be clustered; computing in slots ordered by column sum makes that true for
+ * spread densities, and mi_unpermute restores column order afterwards.
+ * mi_column_order: d_perm[s] = the column placed in operand slot s (ascending
+ * column sum, ties by column index: deterministic), d_inv[c] = slot of column
+ * c (n_cols int32 each); d_spread (2 int32, or NULL) = (min, max) column sum. */
+int mi_column_order(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int32_t* d_perm,
+                    int32_t* d_inv, int32_t* d_spread, void* stream);
+/* mi_unpack_colsum with operand slot s holding column d_perm[s] (NULL =
+ * identity); d_colstat / d_colsum are then in slot order. */
+int mi_unpack_colsum_ordered(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, const int32_t* d_perm,
+                             int8_t* d_kmajor, int64_t ld, void* d_colstat, int32_t* d_colsum, void* stream);
+/* d_out[r][c] = d_in[d_inv[r]][d_inv[c]] for r, c < n_cols (pitches in
+ * elements of esz = 4 or 8 bytes; d_in and d_out must not overlap): a result
+ * computed in slot order (full square, as mi_gram_mi writes it) back in
+ * column order.  HBM-bound, one read and one write of the matrix. */
+int mi_unpermute(const void* d_in, int64_t ld_in, void* d_out, int64_t ld_out, int64_t n_cols, int esz,
+                 const int32_t* d_inv, void* stream);
 /* Packed words of a synthetic dataset.  col_kind[c]: 0 Bernoulli(col_threshold[c]),
  * 1 all zero, 2 all one, 3 col_src[c] XOR Bernoulli(flip_threshold) drawn
  * with flip_seed.  Thresholds are ceil(p * 2^64) (datagen.py:53-55). */
@@ -181,7 +201,8 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * accumulator before FP64-free epilogues; 1 default, 0 off, 2 always),
  * "shard" (8 ranks: 1 = column-group pairs, default; 0 = round robin),
  * "hybrid" (exact-mode tiles off the table path: 0 = FP64, default; 1 = three
- * table gathers + T(c00) computed -- slower on every config measured).  Also
+ * table gathers + T(c00) computed -- slower on every config measured),
+ * "unperm_ctas" (CTAs per SM of mi_unpermute: 1 default, 2 or 4).  Also
  * settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */

@@ -64,6 +64,9 @@ SIGNATURES = {
     "mi_rank_blocks": (_i64, [_i64, _int, _int, _vp, _i64]),
     "mi_unpack_colsum": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "mi_unpack_colsum_blocks": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "mi_column_order": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "mi_unpack_colsum_ordered": (_int, [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "mi_unpermute": (_int, [_vp, _i64, _vp, _i64, _i64, _int, _vp, _vp]),
     "mi_gram_mi": (_int, [_vp, _vp, _i64, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
     "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
@@ -100,6 +103,8 @@ def lib() -> ctypes.CDLL:
                 "(there is no CPU fallback)")
         handle = ctypes.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("MI_B200_LIB") and not hasattr(handle, name):
+                continue  # A/B against an older build that predates this entry point
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

@@ -58,7 +58,7 @@ int env_int(const char* name, int dflt) {
 }
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid;
+        hybrid, unperm_ctas;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -67,7 +67,7 @@ Tuning& tuning() {
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
-                       env_int("MI_B200_HYBRID", 0)};
+                       env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -561,6 +561,64 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
                         ld_out, d_tiles, n_tiles, nullptr, (cudaStream_t)stream);
 }
 
+int mi_column_order(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int32_t* d_perm, int32_t* d_inv,
+                    int32_t* d_spread, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (n_cols > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "n_cols must fit in int32 for a column order");
+    if (!d_words || !d_perm || !d_inv) return fail(MI_ERR_DOMAIN, "d_words, d_perm and d_inv are required");
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    MI_CUDA(launch_column_order(d_words, n_rows, n_cols, d_perm, d_inv, reinterpret_cast<int*>(d_spread),
+                                info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
+}
+
+int mi_unpack_colsum_ordered(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, const int32_t* d_perm,
+                             int8_t* d_kmajor, int64_t ld, void* d_colstat, int32_t* d_colsum, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (ld < mi_kmajor_ld(n_rows) || ld % 128)
+        return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
+                    (long long)mi_kmajor_ld(n_rows));
+    if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    const int64_t nw = (n_rows + 63) / 64;
+    MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, d_kmajor, ld, mi_kmajor_rows(n_cols), d_colsum,
+                                 (ColStat*)d_colstat, xlogx_ptr(d_colstat, n_rows, n_cols),
+                                 blkrange_ptr(d_colstat, n_rows, n_cols), fixr_ptr(d_colstat, n_rows, n_cols),
+                                 operand_fp4(n_rows), nullptr, mi_tile_size(), info.num_sms, (cudaStream_t)stream,
+                                 d_perm));
+    return MI_OK;
+}
+
+int mi_unpermute(const void* d_in, int64_t ld_in, void* d_out, int64_t ld_out, int64_t n_cols, int esz,
+                 const int32_t* d_inv, void* stream) {
+    if (n_cols < 1 || n_cols > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "n_cols must be in [1, 2^31)");
+    if (esz != 4 && esz != 8) return fail(MI_ERR_DOMAIN, "esz must be 4 or 8");
+    if (ld_in < n_cols || ld_out < n_cols) return fail(MI_ERR_DIMENSION, "ld_in and ld_out must be >= n_cols");
+    if (!d_in || !d_out || !d_inv) return fail(MI_ERR_DOMAIN, "d_in, d_out and d_inv are required");
+    if ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out)) % (uintptr_t)esz)
+        return fail(MI_ERR_DOMAIN, "d_in and d_out must be aligned to esz");
+    const char* a0 = static_cast<const char*>(d_in);
+    const char* b0 = static_cast<const char*>(d_out);
+    const int64_t span_in = ((n_cols - 1) * ld_in + n_cols) * esz, span_out = ((n_cols - 1) * ld_out + n_cols) * esz;
+    if (a0 < b0 + span_out && b0 < a0 + span_in) return fail(MI_ERR_DOMAIN, "d_in and d_out must not overlap");
+    DevInfo info;
+    int rc;
+    if ((rc = current_device_info(&info))) return rc;
+    int dev = 0, smem = 0;
+    MI_CUDA(cudaGetDevice(&dev));
+    MI_CUDA(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const int ctas = tuning().unperm_ctas;
+    int per_cta = smem / ctas - 1024;  // leave room for the per-CTA reserve
+    per_cta = per_cta / 16 * 16;
+    MI_CUDA(launch_unpermute(d_in, ld_in, d_out, ld_out, n_cols, esz, d_inv, info.num_sms, per_cta, ctas,
+                             (cudaStream_t)stream));
+    return MI_OK;
+}
+
 }  // extern "C"
 
 int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
@@ -1010,6 +1068,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "pace")) {
         if (value < -1) return fail(MI_ERR_DOMAIN, "pace must be -1 (auto), 0 (off) or a window in k-blocks");
         t.pace = value;
+    } else if (!strcmp(key, "unperm_ctas")) {
+        if (value != 1 && value != 2 && value != 4) return fail(MI_ERR_DOMAIN, "unperm_ctas must be 1, 2 or 4");
+        t.unperm_ctas = value;
     } else if (!strcmp(key, "epi_warps")) {
         if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");
         t.epi_warps = value;
@@ -1036,6 +1097,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "evac")) return t.evac;
     if (!strcmp(key, "shard")) return t.shard;
     if (!strcmp(key, "hybrid")) return t.hybrid;
+    if (!strcmp(key, "unperm_ctas")) return t.unperm_ctas;
     return -1;
 }
 

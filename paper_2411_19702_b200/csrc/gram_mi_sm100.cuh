@@ -113,12 +113,15 @@ __device__ __forceinline__ RowMarg row_marg(const ColS& s, double eN, double dN)
 __device__ __forceinline__ ColS col_s(const ColStat& s) { return ColS{s.v, s.e1, s.e0, s.f1, s.f0, s.q, s.vi, 0}; }
 
 // c * L for one cell; c == 0 contributes exactly 0 (0 * log 0 = 0).
-// LOW: float32 output -- a degree-4 log polynomial (truncation ~2.5e-13
-// relative on |u| <= 2^-8, far below float32's 6e-8) instead of degree 8.
+// LOW: float32 output -- a degree-3 log polynomial (truncation < 1.3e-9
+// absolute in log2 of the mantissa, 0 <= u < 2^-7; the cell weights c / N sum
+// to 1, so < ~1.3e-9 in MI: far below the 1e-6 contract) instead of degree 8.
 template <bool LOW = false>
 __device__ __forceinline__ double cell_term(double c, double eab, double fa, double fb, double fN,
                                             const double2* __restrict__ tab) {
-    const double cs = c > 0.0 ? c : 1.0;
+    // c > 0 ? c : 1 by an integer compare of the bits (c >= 0), off the FP64 pipe
+    const long long cb = __double_as_longlong(c);
+    const double cs = cb != 0 ? c : 1.0;
     const int hi = __double2hiint(cs);
     const int lo = __double2loint(cs);
     const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);  // mantissa in [1, 2)
@@ -126,7 +129,7 @@ __device__ __forceinline__ double cell_term(double c, double eab, double fa, dou
     const double u = fma(m, t.x, -1.0);
     double p;
     if constexpr (LOW) {
-        p = fma(u, kLog2C4, kLog2C3);
+        p = kLog2C3;
     } else {
         p = fma(u, kLog2C8, kLog2C7);
         p = fma(u, p, kLog2C6);

@@ -84,7 +84,17 @@ int gram_mi_tile_size(int cg);
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw,
                                  int8_t* x, int64_t ld, int64_t m_pad, int32_t* colsum,
                                  ColStat* colstat, long long* xlogx, int2* blkrange, float* fixr, bool fp4,
-                                 const uint8_t* block_mask, int tile, int num_sms, cudaStream_t stream);
+                                 const uint8_t* block_mask, int tile, int num_sms, cudaStream_t stream,
+                                 const int32_t* perm = nullptr);
+
+// Column order by column sum (order.cu): perm[s] = column in operand slot s
+// (ascending sum, ties by column index), inv[perm[s]] = s; spread (device
+// int[2], or nullptr) = (min, max) column sum.
+cudaError_t launch_column_order(const uint64_t* words, int64_t n_rows, int64_t m, int32_t* perm, int32_t* inv,
+                                int* spread, int num_sms, cudaStream_t stream);
+// out[r][c] = in[inv[r]][inv[c]] for r, c < m; esz 4 or 8 bytes
+cudaError_t launch_unpermute(const void* in, int64_t ld_in, void* out, int64_t ld_out, int64_t m, int esz,
+                             const int32_t* inv, int num_sms, int smem_bytes, int ctas_per_sm, cudaStream_t stream);
 
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,
                                   const uint64_t* col_threshold, const uint8_t* col_kind,

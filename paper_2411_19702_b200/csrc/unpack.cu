@@ -135,7 +135,8 @@ __device__ __forceinline__ void store_fp4_word(int8_t* dst, uint64_t w) {
 template <bool FP4>
 __global__ void __launch_bounds__(256)
 unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x, int64_t ld,
-              int64_t m_pad, ColStat* __restrict__ colstat, const uint8_t* __restrict__ block_mask, int tile_cols) {
+              int64_t m_pad, ColStat* __restrict__ colstat, const uint8_t* __restrict__ block_mask, int tile_cols,
+              const int32_t* __restrict__ perm) {
     if (block_mask && !block_mask[(int64_t)blockIdx.x * kUnpackCols / tile_cols]) return;  // not this rank's block
     __shared__ __align__(16) uint64_t tile[2][kUnpackCols * kUnpackPitch];
     constexpr int WPK = FP4 ? 4 : 2;           // words per 128-byte k-block row
@@ -150,7 +151,8 @@ unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t*
     const int64_t c0 = (int64_t)blockIdx.x * kUnpackCols;
     const int64_t lc = c0 + ld_col;
     const bool lreal = lc < m;
-    const uint64_t* __restrict__ src = words + (lreal ? lc : 0) * nw;
+    // slot lc holds column perm[lc] (column order by column sum, order.cu) or column lc
+    const uint64_t* __restrict__ src = words + (lreal ? (perm ? (int64_t)__ldg(perm + lc) : lc) : 0) * nw;
     const int64_t wbeg = (int64_t)blockIdx.y * kUnpackTiles * kUnpackWords;
     int ntiles = (int)((wpad - wbeg + kUnpackWords - 1) / kUnpackWords);
     if (ntiles > kUnpackTiles) ntiles = kUnpackTiles;
@@ -212,7 +214,7 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
                                  int64_t ld, int64_t m_pad, int32_t* colsum, ColStat* colstat, long long* xlogx,
                                  int2* blkrange, float* fixr, bool fp4, const uint8_t* block_mask, int tile,
                                  int num_sms,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const int32_t* perm) {
     const int fix_s = xlogx_scale(n_rows);
     {
         int64_t work = xlogx ? n_rows + 1 : 0;
@@ -228,9 +230,9 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
     if (chunks > 65535) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)(m_pad / kUnpackCols), (unsigned)chunks);
     if (fp4)
-        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile);
+        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm);
     else
-        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile);
+        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm);
     int64_t cb = (m_pad + 255) / 256;
     if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
     colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, m_pad, colsum, colstat, fix_s,

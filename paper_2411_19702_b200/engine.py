@@ -88,6 +88,14 @@ class Prepared:
     x: torch.Tensor  # int8 (m_pad, ld)
     colsum: torch.Tensor  # int32 (m_pad,)
     colstat: torch.Tensor  # uint8 workspace (mi_colstat_bytes): marginals + their log2 splits
+    perm: torch.Tensor | None = None  # order "colsum": int32 slot -> column (X, colsum, colstat in slot order)
+    inv: torch.Tensor | None = None   # order "colsum": int32 column -> slot
+
+
+ORDERS = ("natural", "colsum", "auto")
+# measured steps (tools/order_probe.py): config 4 (m = 50,000) colsum 25.3 vs natural 25.9 ms,
+# config 5 (m = 20,000) 64.5 vs 66.5 ms, config 2 (m = 2,000) 0.35 vs 0.11 ms
+AUTO_ORDER_MIN_COLS = 16384
 
 
 def _stream_ptr(device: torch.device) -> int:
@@ -144,16 +152,54 @@ class MIEngine:
         host = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))
         return host.to(self.device, non_blocking=False)
 
-    def prepare(self, words_dev: torch.Tensor, n_rows: int, n_cols: int,
-                rank: int = 0, world: int = 1) -> Prepared:
-        """Kernel 1: unpack the packed columns to the K-major operand and
-        count ones per column (binmat.column_sums).  With world > 1 only the
-        column blocks of rank's tiles are expanded (mi_rank_blocks)."""
+    def _check_words(self, words_dev: torch.Tensor, n_rows: int, n_cols: int) -> None:
         nw = n_words(n_rows)
         if words_dev.device != self.device or words_dev.dtype not in (torch.int64, torch.uint64):
             raise DimensionError("words must be a 64-bit tensor on the engine's device")
         if tuple(words_dev.shape) != (n_cols, nw) or not words_dev.is_contiguous():
             raise DimensionError(f"words must be contiguous with shape {(n_cols, nw)}")
+
+    def column_order(self, words_dev: torch.Tensor, n_rows: int, n_cols: int,
+                     spread: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """(perm, inv): operand slots ordered by column sum (mi_column_order)."""
+        self._check_words(words_dev, n_rows, n_cols)
+        perm = torch.empty((n_cols,), dtype=torch.int32, device=self.device)
+        inv = torch.empty((n_cols,), dtype=torch.int32, device=self.device)
+        nat.check(nat.lib().mi_column_order(words_dev.data_ptr(), n_rows, n_cols, perm.data_ptr(), inv.data_ptr(),
+                                            spread.data_ptr() if spread is not None else None,
+                                            _stream_ptr(self.device)),
+                  "mi_column_order")
+        return perm, inv
+
+    def choose_order(self, words_dev: torch.Tensor, n_rows: int, n_cols: int, world: int = 1) -> str:
+        """The "auto" rule: "colsum" when the column sums are spread wider than
+        the table path's per-tile threshold (so natural-order tiles fall back to
+        the FP64 epilogue) and m >= AUTO_ORDER_MIN_COLS on one GPU; "natural"
+        otherwise.  Below that width the fixed costs (the sort, the m^2
+        unpermute pass) outweigh the epilogue saving ("Column
+        order").  Reads two integers back (one stream sync)."""
+        if world > 1 or n_cols < AUTO_ORDER_MIN_COLS or n_cols <= int(nat.lib().mi_tile_size()):
+            return "natural"
+        spread = torch.empty((2,), dtype=torch.int32, device=self.device)
+        self.column_order(words_dev, n_rows, n_cols, spread)
+        lo, hi = (int(x) for x in spread.cpu())
+        return "colsum" if hi - lo > nat.get_tuning("table_thr") else "natural"
+
+    def prepare(self, words_dev: torch.Tensor, n_rows: int, n_cols: int,
+                rank: int = 0, world: int = 1, order: str = "natural") -> Prepared:
+        """Kernel 1: unpack the packed columns to the K-major operand and
+        count ones per column (binmat.column_sums).  With world > 1 only the
+        column blocks of rank's tiles are expanded (mi_rank_blocks).
+        ``order``: "natural" (slot c = column c), "colsum" (slots ordered by
+        column sum, one GPU only; compute() restores column order), or "auto"
+        (choose_order)."""
+        if order not in ORDERS:
+            raise DomainError(f"order must be one of {ORDERS}, got {order!r}")
+        self._check_words(words_dev, n_rows, n_cols)
+        if order == "auto":
+            order = self.choose_order(words_dev, n_rows, n_cols, world)
+        if order == "colsum" and world > 1:
+            raise DomainError("order='colsum' is single-GPU only (each rank would unpermute the whole matrix)")
         ld, m_pad = self.layout(n_rows, n_cols)
         x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
         colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
@@ -165,6 +211,13 @@ class MIEngine:
             if mask is None:
                 mask = torch.from_numpy(nat.rank_blocks(n_cols, rank, world)).to(self.device)
                 self._tiles[key] = mask
+        if order == "colsum":
+            perm, inv = self.column_order(words_dev, n_rows, n_cols)
+            nat.check(nat.lib().mi_unpack_colsum_ordered(words_dev.data_ptr(), n_rows, n_cols, perm.data_ptr(),
+                                                         x.data_ptr(), ld, colstat.data_ptr(), colsum.data_ptr(),
+                                                         _stream_ptr(self.device)),
+                      "mi_unpack_colsum_ordered")
+            return Prepared(n_rows, n_cols, ld, m_pad, x, colsum, colstat, perm, inv)
         nat.check(nat.lib().mi_unpack_colsum_blocks(words_dev.data_ptr(), n_rows, n_cols, x.data_ptr(), ld,
                                                     colstat.data_ptr(), colsum.data_ptr(),
                                                     mask.data_ptr() if mask is not None else None,
@@ -186,6 +239,8 @@ class MIEngine:
         if kind == nat.MI_OUT_COUNTS:
             mode = nat.MI_MODE_EXACT
         m = prep.n_cols
+        if prep.perm is not None:
+            return self._compute_ordered(prep, mode, eps, diag, kind, out_dtype, tiles, out, packed)
         if packed:
             if out is None:
                 out = torch.empty((m * (m + 1) // 2,), dtype=out_dtype, device=self.device)
@@ -208,10 +263,38 @@ class MIEngine:
                   "mi_gram_mi")
         return out
 
+    def _compute_ordered(self, prep: Prepared, mode: int, eps: float, diag: int, kind: int,
+                         out_dtype: torch.dtype, tiles, out, packed: bool) -> torch.Tensor:
+        """Column-sum order: the fused kernel writes the full matrix in slot
+        order into a scratch matrix, mi_unpermute puts it back in column order."""
+        if packed or tiles is not None:
+            raise DomainError("order='colsum' computes the full matrix: no packed output or tile subsets")
+        m = prep.n_cols
+        if out is None:
+            out = torch.empty((m, m), dtype=out_dtype, device=self.device)
+        if out.dtype != out_dtype or out.dim() != 2 or out.shape[0] < m or out.shape[1] < m \
+                or out.stride(1) != 1 or out.device != self.device:
+            raise DimensionError("out must be a row-major (>= m, >= m) tensor of out_dtype on the device")
+        slot = torch.empty((m, m), dtype=out_dtype, device=self.device)
+        stream = _stream_ptr(self.device)
+        tl = self.tiles(m)
+        nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m, prep.ld,
+                                       mode, eps, diag, kind, slot.data_ptr(), m, tl.data_ptr(), tl.shape[0],
+                                       stream),
+                  "mi_gram_mi")
+        nat.check(nat.lib().mi_unpermute(slot.data_ptr(), m, out.data_ptr(), out.stride(0), m, slot.element_size(),
+                                         prep.inv.data_ptr(), stream),
+                  "mi_unpermute")
+        return out
+
     # ------------------------------------------------------------------ composites
     def all_pairs_device(self, words_dev: torch.Tensor, n_rows: int, n_cols: int, cfg=None,
-                         out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None) -> torch.Tensor:
-        return self.compute(self.prepare(words_dev, n_rows, n_cols), cfg, out_dtype, out=out)
+                         out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
+                         order: str = "natural") -> torch.Tensor:
+        """Device words in, device MI (m x m, column order) out.  ``order``:
+        see prepare() ("natural" keeps results bit-identical to the
+        multi-GPU path's)."""
+        return self.compute(self.prepare(words_dev, n_rows, n_cols, order=order), cfg, out_dtype, out=out)
 
     def all_pairs_bmi(self, path, cfg=None, out_dtype: torch.dtype = torch.float64) -> torch.Tensor:
         """MI straight from a BMI1 file (the reference's packed container,
