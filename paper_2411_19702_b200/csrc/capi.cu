@@ -52,13 +52,15 @@ int cuda_fail(cudaError_t e, const char* what) {
 // Tuning knobs: defaults are the measured best; MI_B200_* env vars
 // or mi_set_tuning() override them.  cta_group 2 = 256 x 256 tiles on a CTA
 // pair (production); 1 = single-SM 128 x 128 tiles.
+constexpr int kMaxIngestStages = 16;
+
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
     return (e && *e) ? atoi(e) : dflt;
 }
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid, unperm_ctas;
+        hybrid, unperm_ctas, ingest;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -67,7 +69,8 @@ Tuning& tuning() {
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
-                       env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 1)};
+                       env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 1),
+                       env_int("MI_B200_INGEST", 4)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -374,6 +377,7 @@ struct Workspace {
     void* out = nullptr; size_t out_cap = 0;
     cudaStream_t copy_stream = nullptr;   // D2H of finished row bands
     cudaEvent_t copy_ev[2] = {nullptr, nullptr};  // the last two D2H copies
+    cudaEvent_t stage_ev[kMaxIngestStages] = {};  // staged path: stage g's tiles are stored
     unsigned int* row_done_h = nullptr;   // pinned, mapped: per tile row completion counts
     unsigned int* row_done_d = nullptr;   // device alias of row_done_h
     size_t row_done_cap = 0;
@@ -403,6 +407,8 @@ void release(Workspace& w) {
     if (w.stream) cudaStreamDestroy(w.stream), w.stream = nullptr;
     if (w.copy_stream) cudaStreamDestroy(w.copy_stream), w.copy_stream = nullptr;
     for (auto& e : w.copy_ev)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    for (auto& e : w.stage_ev)
         if (e) cudaEventDestroy(e), e = nullptr;
     if (w.row_done_h) cudaFreeHost(w.row_done_h), w.row_done_h = nullptr, w.row_done_d = nullptr;
     w.row_done_cap = 0;
@@ -727,6 +733,90 @@ int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_
                                true);
 }
 
+// Staged ingest -> compute -> egress (full-matrix output): the column blocks
+// are cut into S groups; group g's words go H2D and are unpacked, then the
+// tiles whose larger block falls in group g run (all their operands are
+// resident), and the region they complete -- rows [0, c0) x columns [c0, c1)
+// and rows [c0, c1) x columns [0, c1) -- goes D2H on the copy stream while
+// group g + 1 uploads and computes.  The egress (PCIe D2H of m^2 elements,
+// the floor of this call) then starts after 1/S of the upload instead of all
+// of it.
+int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,
+                          double epsilon, int include_diagonal, int out_kind, void* h_out, const DevInfo& info,
+                          int stages) {
+    const int64_t nw = (n_rows + 63) / 64;
+    const int64_t ld = mi_kmajor_ld(n_rows);
+    const int64_t m_pad = mi_kmajor_rows(n_cols);
+    const int tile = mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
+    const int S = (int)(stages < T ? stages : T);
+    const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
+    int rc;
+    if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
+    if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
+    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
+    if ((rc = ensure(&ws.out, &ws.out_cap, (size_t)n_cols * (size_t)n_cols * esz))) return rc;
+    // per-stage tile lists (banded order restricted to J in the group), one upload
+    std::vector<int64_t> blk(S + 1);
+    for (int g = 0; g <= S; ++g) blk[g] = T * g / S;
+    const std::vector<int32_t> all = all_tiles(T, tile_band(), 0);
+    std::vector<int32_t> lists;
+    std::vector<int64_t> first(S + 1, 0);
+    for (int g = 0; g < S; ++g) {
+        first[g] = (int64_t)lists.size() / 2;
+        for (size_t k = 0; k < all.size(); k += 2)
+            if (all[k + 1] >= blk[g] && all[k + 1] < blk[g + 1]) {
+                lists.push_back(all[k]);
+                lists.push_back(all[k + 1]);
+            }
+    }
+    first[S] = (int64_t)lists.size() / 2;
+    if ((rc = ensure(&ws.tiles, &ws.tiles_cap, lists.size() * 4))) return rc;
+    MI_CUDA(cudaMemcpyAsync(ws.tiles, lists.data(), lists.size() * 4, cudaMemcpyHostToDevice, ws.stream));
+    for (int g = 0; g < S; ++g)
+        if (!ws.stage_ev[g]) MI_CUDA(cudaEventCreateWithFlags(&ws.stage_ev[g], cudaEventDisableTiming));
+    ColStat* cs = (ColStat*)ws.colstat;
+    long long* xl = xlogx_ptr(ws.colstat, n_rows, n_cols);
+    int2* br = blkrange_ptr(ws.colstat, n_rows, n_cols);
+    const bool fp4 = operand_fp4(n_rows);
+    MI_CUDA(launch_unpack_prep(n_rows, m_pad, cs, xl, br, fixr_ptr(ws.colstat, n_rows, n_cols), info.num_sms,
+                               ws.stream));
+    const size_t pitch = (size_t)n_cols * esz;
+    for (int g = 0; g < S; ++g) {
+        const int64_t c0 = std::min<int64_t>(blk[g] * tile, n_cols), c1 = std::min<int64_t>(blk[g + 1] * tile, n_cols);
+        MI_CUDA(cudaMemcpyAsync((uint64_t*)ws.words + c0 * nw, h_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
+                                cudaMemcpyHostToDevice, ws.stream));
+        const int64_t u1 = g == S - 1 ? m_pad : blk[g + 1] * tile;
+        MI_CUDA(launch_unpack_range((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
+                                    (int32_t*)ws.colsum, cs, xl ? br : nullptr, fp4, nullptr, tile, blk[g] * tile, u1,
+                                    info.num_sms, ws.stream));
+        if ((rc = launch_fused((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, epsilon, include_diagonal,
+                               out_kind, ws.out, n_cols, (const int32_t*)ws.tiles + 2 * first[g],
+                               first[g + 1] - first[g], nullptr, ws.stream)))
+            return rc;
+        MI_CUDA(cudaEventRecord(ws.stage_ev[g], ws.stream));
+        MI_CUDA(cudaStreamWaitEvent(ws.copy_stream, ws.stage_ev[g], 0));
+        char* ho = (char*)h_out;
+        const char* dv = (const char*)ws.out;
+        if (c0 > 0 && c1 > c0)  // rows above the group, the group's columns
+            MI_CUDA(cudaMemcpy2DAsync(ho + c0 * esz, pitch, dv + c0 * esz, pitch, (size_t)(c1 - c0) * esz,
+                                      (size_t)c0, cudaMemcpyDeviceToHost, ws.copy_stream));
+        // the group's rows, columns [0, c1); one linear copy when they are whole
+        // rows (the last group): 2-D copies run at ~52 GB/s against ~57 GB/s
+        // linear on this link (tools/d2h_2d.py)
+        if (c1 > c0 && c1 == n_cols)
+            MI_CUDA(cudaMemcpyAsync(ho + c0 * pitch, dv + c0 * pitch, (size_t)(c1 - c0) * pitch,
+                                    cudaMemcpyDeviceToHost, ws.copy_stream));
+        else if (c1 > c0)
+            MI_CUDA(cudaMemcpy2DAsync(ho + c0 * pitch, pitch, dv + c0 * pitch, pitch, (size_t)c1 * esz,
+                                      (size_t)(c1 - c0), cudaMemcpyDeviceToHost, ws.copy_stream));
+    }
+    MI_CUDA(cudaStreamSynchronize(ws.copy_stream));
+    MI_CUDA(cudaStreamSynchronize(ws.stream));
+    return MI_OK;
+}
+
 int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
                         int include_diagonal, int out_kind, void* h_out, int device, bool packed) {
     int rc = check_shape(n_rows, n_cols);
@@ -745,6 +835,12 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
     Workspace* ws;
     DevInfo info;
     if ((rc = workspace_for(device, &ws, &info))) return rc;
+    if (!packed && tuning().ingest > 0 && tiles_per_side(n_cols) > 1) {
+        rc = all_pairs_host_staged(*ws, h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out,
+                                   info, tuning().ingest);
+        stamp("done (staged)");
+        return rc;
+    }
     int64_t ld, m_pad;
     if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
     stamp("H2D + unpack enqueued");
@@ -1068,6 +1164,10 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "pace")) {
         if (value < -1) return fail(MI_ERR_DOMAIN, "pace must be -1 (auto), 0 (off) or a window in k-blocks");
         t.pace = value;
+    } else if (!strcmp(key, "ingest")) {
+        if (value < 0 || value > kMaxIngestStages)
+            return fail(MI_ERR_DOMAIN, "ingest must be 0 (row-band egress) or 1..%d stages", kMaxIngestStages);
+        t.ingest = value;
     } else if (!strcmp(key, "unperm_ctas")) {
         if (value != 1 && value != 2 && value != 4) return fail(MI_ERR_DOMAIN, "unperm_ctas must be 1, 2 or 4");
         t.unperm_ctas = value;
@@ -1098,6 +1198,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "shard")) return t.shard;
     if (!strcmp(key, "hybrid")) return t.hybrid;
     if (!strcmp(key, "unperm_ctas")) return t.unperm_ctas;
+    if (!strcmp(key, "ingest")) return t.ingest;
     return -1;
 }
 

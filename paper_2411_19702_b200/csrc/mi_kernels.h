@@ -87,6 +87,17 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
                                  const uint8_t* block_mask, int tile, int num_sms, cudaStream_t stream,
                                  const int32_t* perm = nullptr);
 
+// The same in pieces, for staged ingest: the prologue (per-column counters,
+// block ranges, the fixed-point table) once, then the expansion + column
+// statistics of columns [c_begin, c_end) (c_begin a multiple of 32, c_end <=
+// m_pad) as their words arrive.  blkrange = nullptr when there is no table.
+cudaError_t launch_unpack_prep(int64_t n_rows, int64_t m_pad, ColStat* colstat, long long* xlogx, int2* blkrange,
+                               float* fixr, int num_sms, cudaStream_t stream);
+cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x, int64_t ld,
+                                int64_t m_pad, int32_t* colsum, ColStat* colstat, int2* blkrange, bool fp4,
+                                const uint8_t* block_mask, int tile, int64_t c_begin, int64_t c_end, int num_sms,
+                                cudaStream_t stream, const int32_t* perm = nullptr);
+
 // Column order by column sum (order.cu): perm[s] = column in operand slot s
 // (ascending sum, ties by column index), inv[perm[s]] = s; spread (device
 // int[2], or nullptr) = (min, max) column sum.

@@ -155,10 +155,10 @@ __global__ void __launch_bounds__(512) unpermute_kernel(const T* __restrict__ in
             if (((head * sizeof(T)) & 15) == 0) {
                 const int4* __restrict__ sv = reinterpret_cast<const int4*>(s + head);
                 int4* dv = reinterpret_cast<int4*>(stage + head);
-                // 8 independent 16-byte loads in flight per thread before their
+                // 16 independent 16-byte loads in flight per thread before their
                 // shared-memory stores (a load -> store -> load chain would
                 // leave one load in flight and starve HBM)
-                constexpr int U = 8;
+                constexpr int U = 16;
                 for (int k0 = tid; k0 < nv; k0 += U * nthr) {
                     int4 r[U];
 #pragma unroll
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(512) unpermute_kernel(const T* __restrict__ in
                 // whole row staged: every output vector is written, B per thread
                 // per batch with their index loads issued together
                 const int mv = m / V;
-                constexpr int B = 4;
+                constexpr int B = 8;
                 using IV = typename VecOps<T>::Idx;
                 for (int q0 = tid; q0 < mv; q0 += B * nthr) {
                     IV iv[B];

@@ -136,8 +136,9 @@ template <bool FP4>
 __global__ void __launch_bounds__(256)
 unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x, int64_t ld,
               int64_t m_pad, ColStat* __restrict__ colstat, const uint8_t* __restrict__ block_mask, int tile_cols,
-              const int32_t* __restrict__ perm) {
-    if (block_mask && !block_mask[(int64_t)blockIdx.x * kUnpackCols / tile_cols]) return;  // not this rank's block
+              const int32_t* __restrict__ perm, int64_t col_base) {
+    const int64_t c0 = col_base + (int64_t)blockIdx.x * kUnpackCols;  // first column of this block
+    if (block_mask && !block_mask[c0 / tile_cols]) return;  // not this rank's block
     __shared__ __align__(16) uint64_t tile[2][kUnpackCols * kUnpackPitch];
     constexpr int WPK = FP4 ? 4 : 2;           // words per 128-byte k-block row
     constexpr int KBT = kUnpackWords / WPK;    // k-blocks per tile
@@ -148,7 +149,6 @@ unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t*
     const int64_t kb_stride = m_pad * 128;
     const int ld_col = t >> 3;     // loader: column of the group
     const int ld_sub = t & 7;      // loader: 8 words of the tile row
-    const int64_t c0 = (int64_t)blockIdx.x * kUnpackCols;
     const int64_t lc = c0 + ld_col;
     const bool lreal = lc < m;
     // slot lc holds column perm[lc] (column order by column sum, order.cu) or column lc
@@ -203,11 +203,47 @@ unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t*
 }
 
 // Epilogue of kernel 1: per-column statistics from the finished counts.
-__global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m, int64_t m_pad,
+__global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m, int64_t c_begin, int64_t c_end,
                                                       int32_t* __restrict__ colsum, ColStat* __restrict__ colstat,
                                                       int fix_s, int2* __restrict__ blkrange) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m_pad; c += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t c = c_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c_end;
+         c += (int64_t)gridDim.x * blockDim.x)
         write_colstat(c, (uint32_t)colstat[c].vi, n_rows, c < m, fix_s, colsum, colstat, blkrange);
+}
+
+cudaError_t launch_unpack_prep(int64_t n_rows, int64_t m_pad, ColStat* colstat, long long* xlogx, int2* blkrange,
+                               float* fixr, int num_sms, cudaStream_t stream) {
+    const int fix_s = xlogx_scale(n_rows);
+    int64_t work = xlogx ? n_rows + 1 : 0;
+    if (work < m_pad) work = m_pad;
+    int64_t tb = (work + 255) / 256;
+    if (tb > (int64_t)num_sms * 16) tb = (int64_t)num_sms * 16;
+    unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, xlogx, n_rows, fix_s, blkrange,
+                                                         (xlogx && blkrange) ? (int)(m_pad / 128) : 0,
+                                                         xlogx ? fixr : nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x, int64_t ld,
+                                int64_t m_pad, int32_t* colsum, ColStat* colstat, int2* blkrange, bool fp4,
+                                const uint8_t* block_mask, int tile, int64_t c_begin, int64_t c_end, int num_sms,
+                                cudaStream_t stream, const int32_t* perm) {
+    if (c_begin % kUnpackCols || c_end > m_pad || c_begin >= c_end) return cudaErrorInvalidValue;
+    const int fix_s = xlogx_scale(n_rows);
+    const int64_t wpad = ld / 128 * (fp4 ? 4 : 2);
+    const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);
+    if (chunks > 65535) return cudaErrorInvalidValue;
+    const dim3 grid((unsigned)((c_end - c_begin + kUnpackCols - 1) / kUnpackCols), (unsigned)chunks);
+    if (fp4)
+        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm,
+                                                      c_begin);
+    else
+        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm,
+                                                       c_begin);
+    int64_t cb = (c_end - c_begin + 255) / 256;
+    if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
+    colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, c_begin, c_end, colsum, colstat, fix_s, blkrange);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x,
@@ -215,29 +251,10 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
                                  int2* blkrange, float* fixr, bool fp4, const uint8_t* block_mask, int tile,
                                  int num_sms,
                                  cudaStream_t stream, const int32_t* perm) {
-    const int fix_s = xlogx_scale(n_rows);
-    {
-        int64_t work = xlogx ? n_rows + 1 : 0;
-        if (work < m_pad) work = m_pad;
-        int64_t tb = (work + 255) / 256;
-        if (tb > (int64_t)num_sms * 16) tb = (int64_t)num_sms * 16;
-        unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, xlogx, n_rows, fix_s, blkrange,
-                                                             (xlogx && blkrange) ? (int)(m_pad / 128) : 0,
-                                                             xlogx ? fixr : nullptr);
-    }
-    const int64_t wpad = ld / 128 * (fp4 ? 4 : 2);
-    const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);
-    if (chunks > 65535) return cudaErrorInvalidValue;
-    const dim3 grid((unsigned)(m_pad / kUnpackCols), (unsigned)chunks);
-    if (fp4)
-        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm);
-    else
-        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm);
-    int64_t cb = (m_pad + 255) / 256;
-    if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
-    colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, m_pad, colsum, colstat, fix_s,
-                                                     xlogx ? blkrange : nullptr);
-    return cudaGetLastError();
+    cudaError_t e = launch_unpack_prep(n_rows, m_pad, colstat, xlogx, blkrange, fixr, num_sms, stream);
+    if (e != cudaSuccess) return e;
+    return launch_unpack_range(words, n_rows, m, nw, x, ld, m_pad, colsum, colstat, xlogx ? blkrange : nullptr, fp4,
+                               block_mask, tile, 0, m_pad, num_sms, stream, perm);
 }
 
 }  // namespace mib200

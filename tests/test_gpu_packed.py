@@ -31,3 +31,29 @@ def test_packed_equals_upper_triangle(engine, n, m, dtype):
     assert np.array_equal(unpack_upper(packed, m), full)
     host = engine.all_pairs_host(words, n, m, None, dt, packed=True).numpy()
     assert np.array_equal(host, full[iu])
+
+
+@pytest.mark.parametrize("ingest", [0, 1, 2, 3, 4, 16])
+@pytest.mark.parametrize("n,m", [(100, 7), (777, 300), (4_097, 1_300), (3_000, 2_600), (20_000, 700)])
+def test_staged_host_path_equals_device(engine, ingest, n, m):
+    """mi_all_pairs_host with S staged column groups (upload, unpack, the
+    group's tiles, 2-D egress of the region they complete) or the row-band
+    path (ingest 0): bit-identical to the device path, both dtypes."""
+    from paper_2411_19702_b200 import _native as nat
+
+    rng = np.random.default_rng(n + 7 * m)
+    dens = rng.uniform(0.01, 0.99, m)
+    words = O.pack_bits((rng.random((n, m)) < dens[None, :]).astype(np.uint8))
+    dev = engine.upload(words)
+    old = nat.get_tuning("ingest")
+    try:
+        nat.set_tuning(ingest=ingest)
+        for dt in (torch.float64, torch.float32):
+            full = engine.all_pairs_device(dev, n, m, None, dt).cpu().numpy()
+            pinned = torch.empty((m, m), dtype=dt, pin_memory=True)
+            host = engine.all_pairs_host(words, n, m, None, dt, host_out=pinned).numpy()
+            assert np.array_equal(host, full)
+            pageable = engine.all_pairs_host(words, n, m, None, dt, host_out=torch.empty((m, m), dtype=dt)).numpy()
+            assert np.array_equal(pageable, full)
+    finally:
+        nat.set_tuning(ingest=old)
