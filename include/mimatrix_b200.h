@@ -111,6 +111,16 @@ int mi_unpack_colsum(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, in
 int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor,
                             int64_t ld, void* d_colstat, int32_t* d_colsum, const uint8_t* d_block_mask,
                             void* stream);
+/* mi_unpack_colsum_blocks in pieces, for staged ingest (words arriving by
+ * column groups): mi_unpack_prep once (per-column counters, block ranges, the
+ * fixed-point table), then mi_unpack_colsum_range for columns [c_begin, c_end)
+ * (c_begin a multiple of 32, c_end <= mi_kmajor_rows(n_cols)) once their
+ * words are on the device; the ranges must cover every column before the
+ * tiles that need them run. */
+int mi_unpack_prep(int64_t n_rows, int64_t n_cols, void* d_colstat, void* stream);
+int mi_unpack_colsum_range(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor,
+                           int64_t ld, void* d_colstat, int32_t* d_colsum, const uint8_t* d_block_mask,
+                           int64_t c_begin, int64_t c_end, void* stream);
 /* Fused G11 + MI over the listed upper-triangle tiles; writes each tile and
  * its mirror into d_out (row-major, pitch ld_out elements), or with ld_out =
  * MI_PACKED_UPPER only the elements j >= i, packed (see above). */

@@ -560,6 +560,41 @@ int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_c
     return MI_OK;
 }
 
+int mi_unpack_prep(int64_t n_rows, int64_t n_cols, void* d_colstat, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    MI_CUDA(launch_unpack_prep(n_rows, mi_kmajor_rows(n_cols), (ColStat*)d_colstat,
+                               xlogx_ptr(d_colstat, n_rows, n_cols), blkrange_ptr(d_colstat, n_rows, n_cols),
+                               fixr_ptr(d_colstat, n_rows, n_cols), info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
+}
+
+int mi_unpack_colsum_range(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int8_t* d_kmajor, int64_t ld,
+                           void* d_colstat, int32_t* d_colsum, const uint8_t* d_block_mask, int64_t c_begin,
+                           int64_t c_end, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (ld < mi_kmajor_ld(n_rows) || ld % 128)
+        return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
+                    (long long)mi_kmajor_ld(n_rows));
+    if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
+    const int64_t m_pad = mi_kmajor_rows(n_cols);
+    if (c_begin < 0 || c_begin % 32 || c_end > m_pad || c_begin >= c_end)
+        return fail(MI_ERR_DIMENSION, "column range [%lld, %lld) must start at a multiple of 32 and lie in [0, %lld)",
+                    (long long)c_begin, (long long)c_end, (long long)m_pad);
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    const int64_t nw = (n_rows + 63) / 64;
+    long long* xl = xlogx_ptr(d_colstat, n_rows, n_cols);
+    MI_CUDA(launch_unpack_range(d_words, n_rows, n_cols, nw, d_kmajor, ld, m_pad, d_colsum, (ColStat*)d_colstat,
+                                xl ? blkrange_ptr(d_colstat, n_rows, n_cols) : nullptr, operand_fp4(n_rows),
+                                d_block_mask, mi_tile_size(), c_begin, c_end, info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
+}
+
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld,
                int mode, double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
                const int32_t* d_tiles, int64_t n_tiles, void* stream) {

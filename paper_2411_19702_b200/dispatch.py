@@ -81,6 +81,66 @@ def run_sharded(words: torch.Tensor | None, n_rows: int, n_cols: int,
     return tiles
 
 
+def stage_bounds(n_cols: int, stages: int) -> list[tuple[int, int, int, int]]:
+    """Column groups of the staged broadcast: (first block, end block, first
+    column, end column) per group, blocks of mi_tile_size() columns split as
+    evenly as possible (the C ABI's staged host path cuts them the same way)."""
+    tile = int(nat.lib().mi_tile_size())
+    T = -(-n_cols // tile)
+    S = max(1, min(stages, T))
+    out = []
+    for g in range(S):
+        b0, b1 = T * g // S, T * (g + 1) // S
+        out.append((b0, b1, min(b0 * tile, n_cols), min(b1 * tile, n_cols)))
+    return out
+
+
+def auto_stages(n_cols: int, world: int, num_sms: int) -> int:
+    """Column groups for the staged broadcast: one per 8 tile rounds of a
+    rank's share, at most 4, and none at world 1 (nothing to overlap).  Each
+    extra group costs a partial tile round: measured at world 1
+    (tools/stage_overhead.py) +0.58 ms on config 4 (26.0 ms) but +0.43 ms on
+    config 3 (1.8 ms), so short shares stay in one piece."""
+    if world <= 1:
+        return 1
+    tile = int(nat.lib().mi_tile_size())
+    T = -(-n_cols // tile)
+    rounds = T * (T + 1) // 2 / world / max(1, num_sms // 2)
+    return int(max(1, min(4, rounds // 8)))
+
+
+def run_sharded_staged(words: torch.Tensor | None, n_rows: int, n_cols: int,
+                       begin: Callable[[], object],
+                       stage: Callable[[object, torch.Tensor, int, int, int, np.ndarray, torch.Tensor], None],
+                       out: torch.Tensor, device: torch.device, group=None, stages: int = 4,
+                       src: int = 0) -> np.ndarray:
+    """run_sharded with the broadcast cut into column groups that overlap the
+    compute: every group's words go out as their own asynchronous broadcast,
+    and once group g has arrived, ``stage(state, words, g, b0, b1, tiles_g,
+    out)`` runs this rank's tiles whose larger block J lies in [b0, b1) (all
+    their operands are then present).  ``begin()`` runs first and returns the
+    state handed to every stage call.  Returns this rank's tile list."""
+    rank, world = world_info(group)
+    if rank == src:
+        if words is None:
+            raise ValueError("the source rank must provide the words")
+        buf = words.to(device)
+    else:
+        buf = torch.empty((n_cols, n_words(n_rows)), dtype=torch.int64, device=device)
+    bounds = stage_bounds(n_cols, stages)
+    dist_on = dist.is_available() and dist.is_initialized()
+    works = [dist.broadcast(buf[c0:c1], src=src, group=group, async_op=True) if dist_on and c1 > c0 else None
+             for (_, _, c0, c1) in bounds]
+    tiles = rank_tiles(n_cols, rank, world)
+    state = begin()
+    for g, (b0, b1, c0, c1) in enumerate(bounds):
+        if works[g] is not None:
+            works[g].wait()
+        sel = tiles[(tiles[:, 1] >= b0) & (tiles[:, 1] < b1)] if len(tiles) else tiles
+        stage(state, buf, g, b0, b1, sel, out)
+    return tiles
+
+
 def gather_to_root(out: torch.Tensor, n_cols: int, root: int = 0, group=None) -> torch.Tensor | None:
     """Assemble the full matrix on `root` from every rank's shard.
 
@@ -101,17 +161,39 @@ def gather_to_root(out: torch.Tensor, n_cols: int, root: int = 0, group=None) ->
 
 def mi_all_pairs_sharded(engine, words: torch.Tensor | None, n_rows: int, n_cols: int, cfg=None,
                          out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
-                         group=None, zero_fill: bool = False) -> tuple[torch.Tensor, np.ndarray]:
+                         group=None, zero_fill: bool = False, stages: int | None = None
+                         ) -> tuple[torch.Tensor, np.ndarray]:
     """GPU version: broadcast + unpack + fused Gram/MI over this rank's tiles.
 
     Returns (local output with this rank's tiles and mirrors written, tiles).
     ``zero_fill`` zeroes the rest of the local output, as gather_to_root needs.
+    ``stages`` > 1: the broadcast goes out in that many column groups, each
+    unpacked and its tiles computed as soon as it arrives
+    (run_sharded_staged); the result is bit-identical.  None: auto_stages().
     """
     rank, world = world_info(group)
+    if stages is None:
+        stages = auto_stages(n_cols, world, engine.num_sms)
     if out is None:
         out = (torch.zeros if zero_fill else torch.empty)((n_cols, n_cols), dtype=out_dtype, device=engine.device)
     elif zero_fill:
         out.zero_()
+
+    if stages > 1:
+        tile = int(nat.lib().mi_tile_size())
+
+        def begin():
+            return engine.prepare_begin(n_rows, n_cols)
+
+        def stage(prep, w, g, b0, b1, tiles_g, o):
+            last = b1 * tile >= n_cols
+            engine.prepare_range(prep, w, b0 * tile, prep.m_pad if last else b1 * tile, rank, world)
+            if len(tiles_g):
+                t = torch.from_numpy(np.ascontiguousarray(tiles_g, dtype=np.int32)).to(engine.device)
+                engine.compute(prep, cfg, out_dtype, tiles=t, out=o)
+
+        tiles = run_sharded_staged(words, n_rows, n_cols, begin, stage, out, engine.device, group, stages)
+        return out, tiles
 
     def compute(w, tiles, o):
         prep = engine.prepare(w, n_rows, n_cols, rank, world)  # only this rank's column blocks
@@ -134,11 +216,12 @@ def copy_share_to_host(engine, local: torch.Tensor, n_cols: int, tiles: np.ndarr
 
 def mi_all_pairs_to_host(engine, words: torch.Tensor | None, n_rows: int, n_cols: int, host, cfg=None,
                          out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,
-                         group=None) -> np.ndarray:
+                         group=None, stages: int | None = None) -> np.ndarray:
     """Sharded compute, then every rank writes its share into the shared host
     matrix over its own PCIe link; after the barrier the full matrix is in
     ``host.array`` on every rank of the node."""
-    local, tiles = mi_all_pairs_sharded(engine, words, n_rows, n_cols, cfg, out_dtype, out=out, group=group)
+    local, tiles = mi_all_pairs_sharded(engine, words, n_rows, n_cols, cfg, out_dtype, out=out, group=group,
+                                        stages=stages)
     copy_share_to_host(engine, local, n_cols, tiles, host)
     if dist.is_available() and dist.is_initialized():
         dist.barrier(group=group)

@@ -185,6 +185,45 @@ class MIEngine:
         lo, hi = (int(x) for x in spread.cpu())
         return "colsum" if hi - lo > nat.get_tuning("table_thr") else "natural"
 
+    def _alloc_prepared(self, n_rows: int, n_cols: int):
+        ld, m_pad = self.layout(n_rows, n_cols)
+        x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
+        colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
+        colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_rows, n_cols)),), dtype=torch.uint8, device=self.device)
+        return x, colsum, colstat
+
+    def _rank_mask(self, n_cols: int, rank: int, world: int) -> torch.Tensor | None:
+        if world <= 1:
+            return None
+        key = ("blocks", n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("shard"))
+        mask = self._tiles.get(key)
+        if mask is None:
+            mask = torch.from_numpy(nat.rank_blocks(n_cols, rank, world)).to(self.device)
+            self._tiles[key] = mask
+        return mask
+
+    def prepare_begin(self, n_rows: int, n_cols: int) -> Prepared:
+        """Staged kernel 1, first part (mi_unpack_prep): buffers and the
+        per-call prologue; then prepare_range() per column group as its words
+        arrive (dispatch's staged broadcast)."""
+        x, colsum, colstat = self._alloc_prepared(n_rows, n_cols)
+        ld, m_pad = self.layout(n_rows, n_cols)
+        nat.check(nat.lib().mi_unpack_prep(n_rows, n_cols, colstat.data_ptr(), _stream_ptr(self.device)),
+                  "mi_unpack_prep")
+        return Prepared(n_rows, n_cols, ld, m_pad, x, colsum, colstat)
+
+    def prepare_range(self, prep: Prepared, words_dev: torch.Tensor, c_begin: int, c_end: int,
+                      rank: int = 0, world: int = 1) -> None:
+        """Expand columns [c_begin, c_end) of X (only rank's blocks when world >
+        1) and their statistics (mi_unpack_colsum_range)."""
+        self._check_words(words_dev, prep.n_rows, prep.n_cols)
+        mask = self._rank_mask(prep.n_cols, rank, world)
+        nat.check(nat.lib().mi_unpack_colsum_range(words_dev.data_ptr(), prep.n_rows, prep.n_cols, prep.x.data_ptr(),
+                                                   prep.ld, prep.colstat.data_ptr(), prep.colsum.data_ptr(),
+                                                   mask.data_ptr() if mask is not None else None, c_begin, c_end,
+                                                   _stream_ptr(self.device)),
+                  "mi_unpack_colsum_range")
+
     def prepare(self, words_dev: torch.Tensor, n_rows: int, n_cols: int,
                 rank: int = 0, world: int = 1, order: str = "natural") -> Prepared:
         """Kernel 1: unpack the packed columns to the K-major operand and
@@ -200,17 +239,9 @@ class MIEngine:
             order = self.choose_order(words_dev, n_rows, n_cols, world)
         if order == "colsum" and world > 1:
             raise DomainError("order='colsum' is single-GPU only (each rank would unpermute the whole matrix)")
+        x, colsum, colstat = self._alloc_prepared(n_rows, n_cols)
         ld, m_pad = self.layout(n_rows, n_cols)
-        x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
-        colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
-        colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_rows, n_cols)),), dtype=torch.uint8, device=self.device)
-        mask = None
-        if world > 1:
-            key = ("blocks", n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("shard"))
-            mask = self._tiles.get(key)
-            if mask is None:
-                mask = torch.from_numpy(nat.rank_blocks(n_cols, rank, world)).to(self.device)
-                self._tiles[key] = mask
+        mask = self._rank_mask(n_cols, rank, world)
         if order == "colsum":
             perm, inv = self.column_order(words_dev, n_rows, n_cols)
             nat.check(nat.lib().mi_unpack_colsum_ordered(words_dev.data_ptr(), n_rows, n_cols, perm.data_ptr(),

@@ -45,7 +45,7 @@ def _oracle_compute(n_rows, n_cols):
     return compute
 
 
-def _worker(rank, world, port, n, m, result_q):
+def _worker(rank, world, port, n, m, result_q, stages=1):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -61,7 +61,25 @@ def _worker(rank, world, port, n, m, result_q):
             bits = (rng.random((n, m)) < 0.4).astype(np.uint8)
             words = torch.from_numpy(O.pack_bits(bits).view(np.int64))
         out = torch.zeros((m, m), dtype=torch.float64)
-        tiles = dispatch.run_sharded(words, n, m, _oracle_compute(n, m), out, torch.device("cpu"))
+        if stages == 1:
+            tiles = dispatch.run_sharded(words, n, m, _oracle_compute(n, m), out, torch.device("cpu"))
+        else:
+            compute = _oracle_compute(n, m)
+            seen = []
+
+            def stage(state, w, g, b0, b1, tiles_g, o):
+                # the tiles of this group touch only columns that have arrived:
+                # columns [0, c1) must already hold the source's words
+                c1 = dispatch.stage_bounds(m, stages)[g][3]
+                ref_w = torch.from_numpy(O.pack_bits((np.random.default_rng(11).random((n, m)) < 0.4)
+                                                     .astype(np.uint8)).view(np.int64))
+                assert torch.equal(w[:c1], ref_w[:c1])
+                seen.append(len(tiles_g))
+                compute(w, tiles_g, o)
+
+            tiles = dispatch.run_sharded_staged(words, n, m, lambda: None, stage, out, torch.device("cpu"),
+                                                stages=stages)
+            assert sum(seen) == len(tiles)
         full = dispatch.gather_to_root(out, m)
         if rank == 0:
             ref = O.c_mi_all_pairs(words.numpy().view(np.uint64), n)
@@ -74,12 +92,15 @@ def _worker(rank, world, port, n, m, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,m", [(300, 600), (1000, 300)])
-def test_two_rank_broadcast_shard_gather(n, m):
+@pytest.mark.parametrize("stages", [1, 2, 3])
+@pytest.mark.parametrize("n,m", [(300, 600), (1000, 300), (200, 1100)])
+def test_two_rank_broadcast_shard_gather(n, m, stages):
+    """One broadcast (stages 1) or column-group broadcasts overlapping the
+    per-group compute (dispatch.run_sharded_staged): the same gathered matrix."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, m, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, m, q, stages)) for r in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=180) for _ in procs]

@@ -28,7 +28,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, m, cfg_id, dtype_name, result_q):
+def _worker(rank, world, port, n, m, cfg_id, dtype_name, result_q, stages=1):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -44,7 +44,7 @@ def _worker(rank, world, port, n, m, cfg_id, dtype_name, result_q):
         dtype = getattr(torch, dtype_name)
         words = datagen.generate_words_device(datagen.config_recipe(cfg_id, n, m), eng.device) if rank == 0 else None
         cfg = EngineConfig()
-        local, tiles = dispatch.mi_all_pairs_sharded(eng, words, n, m, cfg, dtype, zero_fill=True)
+        local, tiles = dispatch.mi_all_pairs_sharded(eng, words, n, m, cfg, dtype, zero_fill=True, stages=stages)
         full = dispatch.gather_to_root(local, m)
         torch.cuda.synchronize()
         if rank == 0:
@@ -62,18 +62,19 @@ def _worker(rank, world, port, n, m, cfg_id, dtype_name, result_q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("stages", [1, 4])
 @pytest.mark.parametrize("n,m,cfg_id,dtype", [
     (10_000, 2_000, 2, "float64"),
     (4_097, 1_300, 4, "float32"),
     (1_000, 257, 1, "float64"),
 ])
-def test_two_rank_sharded_gather_matches_single(n, m, cfg_id, dtype):
+def test_two_rank_sharded_gather_matches_single(n, m, cfg_id, dtype, stages):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, m, cfg_id, dtype, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, m, cfg_id, dtype, q, stages)) for r in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in procs]

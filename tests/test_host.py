@@ -207,3 +207,21 @@ def test_product_recipe_agrees_with_oracle(cfg):
 def test_signature_binding_types():
     fn = nat.lib().mi_all_pairs_host
     assert fn.restype is ctypes.c_int and len(fn.argtypes) == 9
+
+
+def test_staged_broadcast_plan():
+    """Column groups of the staged broadcast: cover every block once, in
+    order; auto_stages splits only long per-rank shares (host logic)."""
+    from paper_2411_19702_b200 import dispatch
+
+    for m in (1, 255, 256, 257, 10_000, 50_000):
+        for S in (1, 2, 3, 4, 7):
+            b = dispatch.stage_bounds(m, S)
+            T = -(-m // 256)
+            assert b[0][0] == 0 and b[-1][1] == T and b[-1][3] == m
+            assert all(b[k][1] == b[k + 1][0] and b[k][3] == b[k + 1][2] for k in range(len(b) - 1))
+            assert len(b) == min(S, T)
+    assert dispatch.auto_stages(50_000, 1, 148) == 1
+    assert dispatch.auto_stages(50_000, 8, 148) == 4     # config 4: ~33 rounds per rank
+    assert dispatch.auto_stages(10_000, 8, 148) == 1     # config 3: ~1.4 rounds per rank
+    assert dispatch.auto_stages(10_000, 2, 148) == 1
