@@ -60,7 +60,7 @@ int env_int(const char* name, int dflt) {
 }
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid, unperm_ctas, ingest;
+        hybrid, unperm_ctas, ingest, ingest_split;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -70,7 +70,7 @@ Tuning& tuning() {
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 1),
-                       env_int("MI_B200_INGEST", 4)};
+                       env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -784,8 +784,20 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
     const int64_t m_pad = mi_kmajor_rows(n_cols);
     const int tile = mi_tile_size();
     const int64_t T = tiles_per_side(n_cols);
-    const int S = (int)(stages < T ? stages : T);
+    int S = (int)(stages < T ? stages : T);
     const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
+    // group boundaries in blocks: even (ingest_split 0), or doubling (1:
+    // T/2^(S-1), ..., T/4, T/2, T).  Doubling starts the egress after a small
+    // first upload and leaves half of the matrix to the last group, whose
+    // rows go down as one linear copy; even groups make 3/4 of it 2-D copies.
+    std::vector<int64_t> blk;
+    blk.push_back(0);
+    for (int g = 1; g <= S; ++g) {
+        const int64_t b = tuning().ingest_split ? (T >> (S - g)) : T * g / S;
+        if (b > blk.back()) blk.push_back(b);
+    }
+    if (blk.back() != T) blk.push_back(T);
+    S = (int)blk.size() - 1;
     int rc;
     if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
     if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
@@ -793,8 +805,6 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
     if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
     if ((rc = ensure(&ws.out, &ws.out_cap, (size_t)n_cols * (size_t)n_cols * esz))) return rc;
     // per-stage tile lists (banded order restricted to J in the group), one upload
-    std::vector<int64_t> blk(S + 1);
-    for (int g = 0; g <= S; ++g) blk[g] = T * g / S;
     const std::vector<int32_t> all = all_tiles(T, tile_band(), 0);
     std::vector<int32_t> lists;
     std::vector<int64_t> first(S + 1, 0);
@@ -1203,6 +1213,9 @@ int mi_set_tuning(const char* key, int value) {
         if (value < 0 || value > kMaxIngestStages)
             return fail(MI_ERR_DOMAIN, "ingest must be 0 (row-band egress) or 1..%d stages", kMaxIngestStages);
         t.ingest = value;
+    } else if (!strcmp(key, "ingest_split")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "ingest_split must be 0 (even) or 1 (doubling)");
+        t.ingest_split = value;
     } else if (!strcmp(key, "unperm_ctas")) {
         if (value != 1 && value != 2 && value != 4) return fail(MI_ERR_DOMAIN, "unperm_ctas must be 1, 2 or 4");
         t.unperm_ctas = value;
@@ -1234,6 +1247,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "hybrid")) return t.hybrid;
     if (!strcmp(key, "unperm_ctas")) return t.unperm_ctas;
     if (!strcmp(key, "ingest")) return t.ingest;
+    if (!strcmp(key, "ingest_split")) return t.ingest_split;
     return -1;
 }
 
