@@ -50,7 +50,8 @@ def test_unpermute_matches_indexing(engine, dtype):
 
     dev = engine.device
     g = torch.Generator(device="cpu").manual_seed(5)
-    for m, pad_in, pad_out in ((1, 0, 0), (2, 1, 0), (3, 0, 5), (255, 0, 0), (257, 3, 1), (777, 0, 2), (4100, 0, 0)):
+    for m, pad_in, pad_out in ((1, 0, 0), (2, 1, 0), (3, 0, 5), (255, 0, 0), (257, 3, 1), (777, 0, 2), (4100, 0, 0),
+                               (8, 0, 0), (148, 4, 0), (1000, 0, 4), (1002, 2, 2), (10_000, 0, 0), (150, 0, 0)):
         src = torch.randn((m, m + pad_in), generator=g).to(dtype if dtype != torch.int32 else torch.float64)
         if dtype == torch.int32:
             src = (src * 1e6).to(torch.int32)
