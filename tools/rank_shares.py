@@ -1,0 +1,53 @@
+"""Per-rank compute of the multi-GPU dealing, measured one rank at a time on
+one GPU (ranks never wait on each other: each runs its own partial unpack and
+its own tile list).  Reports, per world size, every rank's step time (partial
+unpack + fused kernel over its tiles) and the compute-only strong-scaling
+efficiency T(1) / (world * max_r T_r).  The broadcast (one NCCL broadcast of
+the packed words) is not included -- it needs real NVLink peers.
+    python tools/rank_shares.py --configs 3,4 --worlds 2,4,8"""
+import argparse, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2411_19702_b200 import MIEngine, datagen
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="3,4")
+ap.add_argument("--worlds", default="2,4,8")
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+eng = MIEngine.get(0)
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=eng.device)
+
+
+def timed(fn):
+    fn(); torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(a.reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); fn(); e1.record(); e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
+
+
+for cfg in [int(x) for x in a.configs.split(",")]:
+    rec = datagen.config_recipe(cfg)
+    n, m = rec["n"], rec["m"]
+    dt = torch.float64 if datagen.CONFIGS[cfg]["out"] == "float64" else torch.float32
+    w = datagen.generate_words_device(rec, eng.device)
+    out = torch.empty((m, m), dtype=dt, device=eng.device)
+
+    def step(rank, world):
+        prep = eng.prepare(w, n, m, rank, world)
+        eng.compute(prep, None, dt, tiles=eng.tiles(m, rank, world), out=out)
+
+    t1 = timed(lambda: step(0, 1))
+    print(json.dumps({"cfg": cfg, "world": 1, "ms": round(t1, 3)}), flush=True)
+    for world in [int(x) for x in a.worlds.split(",")]:
+        ts = [timed(lambda r=r: step(r, world)) for r in range(world)]
+        tiles = [int(eng.tiles(m, r, world).shape[0]) for r in range(world)]
+        print(json.dumps({"cfg": cfg, "world": world, "rank_ms": [round(t, 3) for t in ts], "tiles": tiles,
+                          "max_ms": round(max(ts), 3), "compute_efficiency": round(t1 / (world * max(ts)), 3)}),
+              flush=True)
+    del out, w
+    torch.cuda.empty_cache()
