@@ -348,15 +348,49 @@ std::vector<int32_t> rank_tiles(int64_t T, int rank, int world, int band) {
         auto group = [&](int64_t b) { return (int)((b * 4) / T); };
         static const int pairs[8][4] = {{0, 1, -1, -1}, {0, 2, -1, -1}, {0, 3, -1, -1}, {1, 2, -1, -1},
                                         {1, 3, -1, -1}, {2, 3, -1, -1}, {0, 0, 3, 3}, {1, 1, 2, 2}};
-        const int* pr = pairs[rank];
+        std::vector<std::vector<int32_t>> share(8);
         for (int64_t k = 0; k < total; ++k) {
             const int gi = group(all[2 * k]), gj = group(all[2 * k + 1]);
-            if ((gi == pr[0] && gj == pr[1]) || (pr[2] >= 0 && gi == pr[2] && gj == pr[3])) {
-                v.push_back(all[2 * k]);
-                v.push_back(all[2 * k + 1]);
+            for (int r = 0; r < 8; ++r) {
+                const int* pr = pairs[r];
+                if ((gi == pr[0] && gj == pr[1]) || (pr[2] >= 0 && gi == pr[2] && gj == pr[3])) {
+                    share[r].push_back(all[2 * k]);
+                    share[r].push_back(all[2 * k + 1]);
+                    break;
+                }
             }
         }
-        return v;
+        // The two diagonal-group ranks hold s(s + 1) tiles against s^2: hand
+        // their surplus (from the end of their lists) to off-diagonal ranks
+        // that already hold that group's blocks -- no extra unpack -- always
+        // to the least loaded one, until no rank exceeds ceil(total / 8).
+        const size_t cap = (size_t)((total + 7) / 8);
+        auto holds = [&](int r, int g) { return pairs[r][0] == g || pairs[r][1] == g; };
+        for (int d = 6; d < 8; ++d) {
+            while (share[d].size() / 2 > cap) {
+                int best_r = -1;
+                int64_t best_k = -1;
+                for (int gsel = 0; gsel < 2; ++gsel) {
+                    const int g = pairs[d][2 * gsel];
+                    int r_min = -1;
+                    for (int r = 0; r < 6; ++r)
+                        if (holds(r, g) && (r_min < 0 || share[r].size() < share[r_min].size())) r_min = r;
+                    if (r_min < 0 || share[r_min].size() / 2 >= cap) continue;
+                    if (best_r >= 0 && share[best_r].size() <= share[r_min].size()) continue;
+                    for (int64_t k = (int64_t)share[d].size() / 2 - 1; k >= 0; --k)
+                        if (group(share[d][2 * k]) == g) {
+                            best_r = r_min;
+                            best_k = k;
+                            break;
+                        }
+                }
+                if (best_r < 0) break;
+                share[best_r].push_back(share[d][2 * best_k]);
+                share[best_r].push_back(share[d][2 * best_k + 1]);
+                share[d].erase(share[d].begin() + 2 * best_k, share[d].begin() + 2 * best_k + 2);
+            }
+        }
+        return share[rank];
     }
     for (int64_t g = rank; g < total; g += world) {
         v.push_back(all[2 * g]);

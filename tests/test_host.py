@@ -74,7 +74,8 @@ def test_tile_partition_covers_triangle_once(m, world):
             assert (I, J) not in seen, "tile dealt twice"
             seen[(I, J)] = r
     assert len(seen) == T * (T + 1) // 2
-    if world == 8 and T >= 8:  # column-group pairs: s^2 vs s^2 + s tiles, s ~ T/4
+    if world == 8 and T >= 8:  # column-group pairs, the diagonal ranks' surplus handed on
+        assert max(counts) <= -(-len(seen) // 8), "a share above ceil(tiles / 8)"
         assert max(counts) - min(counts) <= T // 4 + 2, "unbalanced shares"
     else:
         assert max(counts) - min(counts) <= 1, "unbalanced shares"
