@@ -144,14 +144,6 @@ __global__ void __launch_bounds__(512) unpermute_kernel(const T* __restrict__ in
     for (int r = blockIdx.x; r < m; r += gridDim.x) {
         const T* __restrict__ src = in + (int64_t)__ldg(inv + r) * ld_in;
         T* __restrict__ dst = out + (int64_t)r * ld_out;
-        // pull this CTA's next source row into L2 while this row is staged and
-        // gathered: its staging then reads at L2 latency instead of DRAM's
-        if (r + (int)gridDim.x < m) {
-            const char* nxt = reinterpret_cast<const char*>(in + (int64_t)__ldg(inv + r + gridDim.x) * ld_in);
-            const int64_t bytes = (int64_t)m * sizeof(T);
-            for (int64_t o = (int64_t)tid * 128; o < bytes; o += (int64_t)nthr * 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(nxt + o));
-        }
         for (int s0 = 0; s0 < m; s0 += chunk) {
             const int n = min(chunk, m - s0);
             __syncthreads();  // the previous pass's gathers are done with `stage`
