@@ -74,11 +74,18 @@ __device__ __forceinline__ void write_colstat(int64_t c, uint32_t cnt, int64_t n
     st.vi = (int)cnt;
     st.pad = 0;
     st.q = fix_xlog2x(cnt, fix_s, kFixR, kFixLG) + fix_xlog2x((unsigned)v0, fix_s, kFixR, kFixLG);
-    if (blkrange && real) {
-        atomicMin(&blkrange[c / 128].x, (int)cnt);
-        atomicMax(&blkrange[c / 128].y, (int)cnt);
-    }
     colstat[c] = st;
+    if (blkrange) {
+        // per-128-column (min, max) of the real columns: one atomic pair per
+        // warp (its 32 columns lie in one block) instead of one per column
+        int lo = real ? (int)cnt : 0x7FFFFFFF, hi = real ? (int)cnt : -1;
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if ((threadIdx.x & 31) == 0 && hi >= 0) {
+            atomicMin(&blkrange[c / 128].x, lo);
+            atomicMax(&blkrange[c / 128].y, hi);
+        }
+    }
 }
 
 // Expansion: block (g, k) owns 32 columns c0 = 32 g .. c0 + 31 and K chunk k
@@ -202,6 +209,55 @@ unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t*
     if (ld_sub == 0 && cnt) atomicAdd(&colstat[lc].vi, (int)cnt);
 }
 
+// e2m1 expansion without shared memory.  Thread (c, j) -- c one of the
+// block's 64 columns (8 per warp), j = lane & 3 the word within a k-block --
+// loads word 4 kb + j of column c (8 bytes: a column's four lanes read one
+// full 32-byte sector) and stores its 32 bytes of nibbles with one STG.256;
+// the warp's 8 columns x 128 bytes are one contiguous 1 KB run of X.  kUnr
+// k-blocks are loaded before any is expanded, so every thread keeps kUnr
+// loads in flight.  (The staged kernel above spends its time in the L1/shared
+// pipeline -- cp.async of 8-byte pieces, then shared-memory reads -- at ~2.7
+// TB/s of writes; this box writes HBM at ~7 TB/s, tools/micro/write_bw.cu.)
+constexpr int kDirectCols = 64;  // columns per block (8 warps x 8)
+template <int kDirectKb, int kUnr>
+__global__ void __launch_bounds__(256)
+unpack_fp4_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x,
+                         int64_t nkb, int64_t m_pad, ColStat* __restrict__ colstat,
+                         const uint8_t* __restrict__ block_mask, int tile_cols, const int32_t* __restrict__ perm,
+                         int64_t col_base, int64_t col_end) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane & 3;
+    const int64_t c = col_base + (int64_t)blockIdx.x * kDirectCols + warp * 8 + (lane >> 2);
+    // no early return: the count reduction below shuffles across the warp
+    const bool active = c < col_end && (!block_mask || block_mask[c / tile_cols]);
+    const bool real = active && c < m;
+    const uint64_t* __restrict__ src = words + (real ? (perm ? (int64_t)__ldg(perm + c) : c) : 0) * nw;
+    const int64_t kb_stride = m_pad * 128;
+    int8_t* const xc = x + c * 128 + j * 32;
+    const int64_t kb0 = (int64_t)blockIdx.y * kDirectKb;
+    const int64_t kb1 = kb0 + kDirectKb < nkb ? kb0 + kDirectKb : nkb;
+    uint32_t cnt = 0;
+    for (int64_t kb = kb0; kb < kb1; kb += kUnr) {
+        uint64_t wv[kUnr];
+#pragma unroll
+        for (int u = 0; u < kUnr; ++u) {
+            const int64_t w = 4 * (kb + u) + j;
+            wv[u] = (real && kb + u < kb1 && w < nw) ? __ldcs(reinterpret_cast<const unsigned long long*>(src + w))
+                                                     : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnr; ++u) {
+            if (active && kb + u < kb1) {
+                cnt += __popcll(wv[u]);
+                store_fp4_word(xc + (kb + u) * kb_stride, wv[u]);
+            }
+        }
+    }
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+    if (j == 0 && real && cnt) atomicAdd(&colstat[c].vi, (int)cnt);
+}
+
 // Epilogue of kernel 1: per-column statistics from the finished counts.
 __global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m, int64_t c_begin, int64_t c_end,
                                                       int32_t* __restrict__ colsum, ColStat* __restrict__ colstat,
@@ -234,10 +290,14 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
     const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);
     if (chunks > 65535) return cudaErrorInvalidValue;
     const dim3 grid((unsigned)((c_end - c_begin + kUnpackCols - 1) / kUnpackCols), (unsigned)chunks);
-    if (fp4)
-        unpack_kernel<true><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm,
-                                                      c_begin);
-    else
+    if (fp4) {
+        const int64_t nkb = ld / 128;
+        constexpr int KB = 32, UNR = 8;  // tools/unpack_bench.py sweep (r01h): best across configs 3-5
+        const dim3 g2((unsigned)((c_end - c_begin + kDirectCols - 1) / kDirectCols), (unsigned)((nkb + KB - 1) / KB));
+        if (g2.y > 65535) return cudaErrorInvalidValue;
+        unpack_fp4_direct_kernel<KB, UNR><<<g2, 256, 0, stream>>>(words, m, nw, x, nkb, m_pad, colstat, block_mask,
+                                                                   tile, perm, c_begin, c_end);
+    } else
         unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm,
                                                        c_begin);
     int64_t cb = (c_end - c_begin + 255) / 256;
