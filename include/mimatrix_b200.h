@@ -215,7 +215,8 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * "unperm_ctas" (CTAs per SM of mi_unpermute: 1 default, 2 or 4), "ingest"
  * (mi_all_pairs_host: S = 1..16 column groups uploaded, unpacked, computed and
  * copied back in a pipeline, default 4; 0 = one upload, row-band egress),
- * "ingest_split" (0 = even group sizes, default; 1 = doubling).  Also
+ * "ingest_split" (0 = even group sizes, default; 1 = doubling), "serp" (1 =
+ * odd tile rounds sweep K backwards for L2 reuse across rounds; 0 default).  Also
  * settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */

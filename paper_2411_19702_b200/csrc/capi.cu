@@ -60,7 +60,7 @@ int env_int(const char* name, int dflt) {
 }
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid, unperm_ctas, ingest, ingest_split;
+        hybrid, unperm_ctas, ingest, ingest_split, serp;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -70,7 +70,8 @@ Tuning& tuning() {
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 1),
-                       env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0)};
+                       env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
+                       env_int("MI_B200_SERP", 0)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -736,6 +737,7 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     int dev = 0;
     MI_CUDA(cudaGetDevice(&dev));
     p.evac = tuning().evac;
+    p.serp = tuning().serp;
     p.pace = nullptr;
     p.pace_window = pace_window(n_tiles, p.num_k_blocks, info.num_sms);
     if (p.pace_window > 0 && (rc = pace_slots(dev, &p.pace))) return rc;
@@ -1247,6 +1249,9 @@ int mi_set_tuning(const char* key, int value) {
         if (value < 0 || value > kMaxIngestStages)
             return fail(MI_ERR_DOMAIN, "ingest must be 0 (row-band egress) or 1..%d stages", kMaxIngestStages);
         t.ingest = value;
+    } else if (!strcmp(key, "serp")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "serp must be 0 or 1");
+        t.serp = value;
     } else if (!strcmp(key, "ingest_split")) {
         if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "ingest_split must be 0 (even) or 1 (doubling)");
         t.ingest_split = value;
@@ -1282,6 +1287,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "unperm_ctas")) return t.unperm_ctas;
     if (!strcmp(key, "ingest")) return t.ingest;
     if (!strcmp(key, "ingest_split")) return t.ingest_split;
+    if (!strcmp(key, "serp")) return t.serp;
     return -1;
 }
 

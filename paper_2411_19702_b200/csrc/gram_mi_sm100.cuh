@@ -371,11 +371,17 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
 
 struct TileWalk {
     // Linear walk over (my tile, k-block) pairs: step g -> tile index, k-block.
-    int cluster, n_clusters, n_tiles, nkb;
+    // serp: odd tile rounds sweep K backwards, so a round starts on the
+    // k-blocks the previous round read last -- still in L2 for the column
+    // blocks the two rounds share.  (The MMA's accumulate flag counts steps,
+    // not k-block indices, so the order of a tile's k-blocks is free: the
+    // counts are exact integers either way.)
+    int cluster, n_clusters, n_tiles, nkb, serp;
     __device__ __forceinline__ bool at(long long g, int& t, int& kb) const {
         const long long it = g / nkb;
         t = cluster + (int)it * n_clusters;
-        kb = (int)(g - it * nkb);
+        const int k = (int)(g - it * nkb);
+        kb = (serp & (int)it) ? nkb - 1 - k : k;
         return t < n_tiles;
     }
 };
@@ -529,7 +535,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     }
 
     const int nkb = p.num_k_blocks;
-    const TileWalk walk{cluster, n_clusters, p.n_full, nkb};
+    const TileWalk walk{cluster, n_clusters, p.n_full, nkb, p.serp & 1};
     // this cluster's split tail unit, if any
     const int n_tail_units = (p.n_tiles - p.n_full) * p.tail_split;
     const bool has_tail = p.tail_split > 1 && cluster < n_tail_units;

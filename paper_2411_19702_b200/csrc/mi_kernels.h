@@ -56,6 +56,7 @@ struct GramMiParams {
     //    * 2 + rank] (zeroed by the host before the launch); units c <
     //    tail_epi then wait for all tail_split partials and run the epilogue
     //    of column slice c (TS / tail_epi wide) on their sum.
+    int serp;               // 1: odd tile rounds sweep K backwards (L2 reuse across rounds)
     int evac;               // fp4: evacuate the accumulator before the epilogue (0 off, 1 FP64-free
                             // epilogues, 2 always)
     int n_full;
