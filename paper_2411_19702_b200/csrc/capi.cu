@@ -864,10 +864,22 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
     MI_CUDA(launch_unpack_prep(n_rows, m_pad, cs, xl, br, fixr_ptr(ws.colstat, n_rows, n_cols), info.num_sms,
                                ws.stream));
     const size_t pitch = (size_t)n_cols * esz;
+    // MI_B200_TIMELINE=1: per-stage event timeline on stderr (experiments only)
+    const bool tl_on = env_int("MI_B200_TIMELINE", 0) != 0;
+    std::vector<cudaEvent_t> tl;
+    auto mark = [&](cudaStream_t st) {
+        if (!tl_on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tl.push_back(e);
+    };
+    mark(ws.stream);
     for (int g = 0; g < S; ++g) {
         const int64_t c0 = std::min<int64_t>(blk[g] * tile, n_cols), c1 = std::min<int64_t>(blk[g + 1] * tile, n_cols);
         MI_CUDA(cudaMemcpyAsync((uint64_t*)ws.words + c0 * nw, h_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
                                 cudaMemcpyHostToDevice, ws.stream));
+        mark(ws.stream);  // H2D g done
         const int64_t u1 = g == S - 1 ? m_pad : blk[g + 1] * tile;
         MI_CUDA(launch_unpack_range((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
                                     (int32_t*)ws.colsum, cs, xl ? br : nullptr, fp4, nullptr, tile, blk[g] * tile, u1,
@@ -877,7 +889,9 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
                                first[g + 1] - first[g], nullptr, ws.stream)))
             return rc;
         MI_CUDA(cudaEventRecord(ws.stage_ev[g], ws.stream));
+        mark(ws.stream);  // compute g done
         MI_CUDA(cudaStreamWaitEvent(ws.copy_stream, ws.stage_ev[g], 0));
+        mark(ws.copy_stream);  // D2H g may start
         char* ho = (char*)h_out;
         const char* dv = (const char*)ws.out;
         if (c0 > 0 && c1 > c0)  // rows above the group, the group's columns
@@ -892,9 +906,19 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
         else if (c1 > c0)
             MI_CUDA(cudaMemcpy2DAsync(ho + c0 * pitch, pitch, dv + c0 * pitch, pitch, (size_t)c1 * esz,
                                       (size_t)(c1 - c0), cudaMemcpyDeviceToHost, ws.copy_stream));
+        mark(ws.copy_stream);  // D2H g done
     }
     MI_CUDA(cudaStreamSynchronize(ws.copy_stream));
     MI_CUDA(cudaStreamSynchronize(ws.stream));
+    if (tl_on) {
+        for (size_t k = 1; k < tl.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl[0], tl[k]);
+            static const char* what[4] = {"H2D done", "compute done", "D2H start", "D2H done"};
+            fprintf(stderr, "[timeline] stage %zu %-12s %8.3f ms\n", (k - 1) / 4, what[(k - 1) % 4], ms);
+        }
+        for (cudaEvent_t e : tl) cudaEventDestroy(e);
+    }
     return MI_OK;
 }
 
