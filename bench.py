@@ -223,8 +223,8 @@ def run_reference(args):
     rec = O.config_recipe(args.config)
     n, m = rec["n"], rec["m"]
     threads = O.c_num_threads()
-    # size one step to ~ (a few minutes / (K + W)) of CPU work
-    budget = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    # size one step to ~ (two minutes / (K + W)) of CPU work
+    budget = max(0.25, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     per_pair_probe = None
     import numpy as np
 
@@ -238,6 +238,15 @@ def run_reference(args):
     ms = max(probe_ms, min(m, int(math.sqrt(2.0 * budget / per_pair_probe))))
     cols = sorted(rng.choice(m, ms, replace=False).tolist()) if ms < m else None
     words = O.c_generate_config_words(rec, cols)
+    # the small probe misjudges a wide sample's cost (thread start-up, cache
+    # effects): time one run at the chosen width and rescale the sample once
+    t0 = time.perf_counter()
+    O.c_mi_all_pairs(words, n)
+    t_first = time.perf_counter() - t0
+    if not 0.8 * budget <= t_first <= 1.2 * budget:
+        ms = max(probe_ms, min(m, int(ms * math.sqrt(budget / t_first))))
+        cols = sorted(rng.choice(m, ms, replace=False).tolist()) if ms < m else None
+        words = O.c_generate_config_words(rec, cols)
     for _ in range(args.warmup):
         O.c_mi_all_pairs(words, n)
     times = []
