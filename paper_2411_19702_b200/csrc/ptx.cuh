@@ -78,12 +78,29 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: a waiting warp is parked until the
+// phase completes (or the hint, in ns, runs out) instead of re-polling.  The
+// fused kernel's waits are long (the epilogue warps wait a whole tile for the
+// accumulator, the MMA warp a whole FP64 epilogue for its release), and the
+// polling loops were ~40% of all executed instructions at config 4 (ncu),
+// issue slots taken from the epilogue warps on the same scheduler.
+__device__ __forceinline__ bool mbar_try_wait_suspend(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
 // Wait for the phase with the given parity to complete.  A watchdog turns a
 // protocol bug into a trap (a reported launch error) instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
-    while (!mbar_try_wait(bar, parity)) {
+    while (!mbar_try_wait_suspend(bar, parity)) {
         if (clock64() - t0 > (long long)20000000000LL) {  // ~10 s at 2 GHz
             __trap();
         }
