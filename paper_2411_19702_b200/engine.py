@@ -318,6 +318,33 @@ class MIEngine:
                   "mi_unpermute")
         return out
 
+    def compute_slot_order(self, prep: Prepared, cfg=None, out_dtype: torch.dtype = torch.float64,
+                           out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+        """The column-sum-ordered result without the unpermute pass: (S, perm)
+        with S[a, b] = MI(perm[a], perm[b]).  For consumers that only need
+        pairs and their values (thresholds, top-k), this skips the m^2 pass
+        (config 4: 19.5 ms of fused kernel instead of 19.5 + 4.6)."""
+        if prep.perm is None:
+            raise DomainError("compute_slot_order needs a prepare(order='colsum') operand")
+        if out_dtype not in _OUT_KIND:
+            raise DomainError(f"out_dtype must be float64, float32 or int32, got {out_dtype}")
+        mode, eps, diag = _config_fields(cfg)
+        kind = _OUT_KIND[out_dtype]
+        if kind == nat.MI_OUT_COUNTS:
+            mode = nat.MI_MODE_EXACT
+        m = prep.n_cols
+        if out is None:
+            out = torch.empty((m, m), dtype=out_dtype, device=self.device)
+        if out.dtype != out_dtype or out.dim() != 2 or out.shape[0] < m or out.shape[1] < m \
+                or out.stride(1) != 1 or out.device != self.device:
+            raise DimensionError("out must be a row-major (>= m, >= m) tensor of out_dtype on the device")
+        tl = self.tiles(m)
+        nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m, prep.ld,
+                                       mode, eps, diag, kind, out.data_ptr(), out.stride(0), tl.data_ptr(),
+                                       tl.shape[0], _stream_ptr(self.device)),
+                  "mi_gram_mi")
+        return out, prep.perm
+
     # ------------------------------------------------------------------ composites
     def all_pairs_device(self, words_dev: torch.Tensor, n_rows: int, n_cols: int, cfg=None,
                          out_dtype: torch.dtype = torch.float64, out: torch.Tensor | None = None,

@@ -205,3 +205,19 @@ def test_colsum_order_full_config(engine, cfg):
     assert float(np.max(np.abs(got - O.c_mi_all_pairs(wS, n)))) < tol
     del b, words
     torch.cuda.empty_cache()
+
+
+def test_slot_order_output(engine):
+    """compute_slot_order: S[a, b] = MI(perm[a], perm[b]) without the unpermute."""
+    from paper_2411_19702_b200.errors import DomainError
+
+    n, m = 3000, 900
+    words = spread_words(n, m, 21)
+    wd = engine.upload(words)
+    full = engine.all_pairs_device(wd, n, m, order="colsum").cpu().numpy()
+    prep = engine.prepare(wd, n, m, order="colsum")
+    S, perm = engine.compute_slot_order(prep)
+    S, perm = S.cpu().numpy(), perm.cpu().numpy().astype(np.int64)
+    assert np.array_equal(S, full[np.ix_(perm, perm)])
+    with pytest.raises(DomainError):
+        engine.compute_slot_order(engine.prepare(wd, n, m))
