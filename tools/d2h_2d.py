@@ -34,9 +34,9 @@ ev = torch.cuda.Event()
 
 def two(w):
     half = m // 2
-    rt.cudaMemcpy2DAsync(host.data_ptr(), pitch, dev.data_ptr(), pitch, w * 8, half, K, st)
-    ev.record(torch.cuda.current_stream())
+    ev.record(torch.cuda.current_stream())  # both copies start together
     s2.wait_event(ev)
+    rt.cudaMemcpy2DAsync(host.data_ptr(), pitch, dev.data_ptr(), pitch, w * 8, half, K, st)
     rt.cudaMemcpy2DAsync(host.data_ptr() + half * pitch, pitch, dev.data_ptr() + half * pitch, pitch, w * 8,
                          m - half, K, s2.cuda_stream)
     e2 = torch.cuda.Event(); e2.record(s2); torch.cuda.current_stream().wait_event(e2)
@@ -49,9 +49,9 @@ for w in (10000, 2500):
 
 def two1d():
     half = m * m // 2 * 8
-    rt.cudaMemcpyAsync(host.data_ptr(), dev.data_ptr(), half, K, st)
     ev.record(torch.cuda.current_stream())
     s2.wait_event(ev)
+    rt.cudaMemcpyAsync(host.data_ptr(), dev.data_ptr(), half, K, st)
     rt.cudaMemcpyAsync(host.data_ptr() + half, dev.data_ptr() + half, half, K, s2.cuda_stream)
     e2 = torch.cuda.Event(); e2.record(s2); torch.cuda.current_stream().wait_event(e2)
 
