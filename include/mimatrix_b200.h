@@ -18,6 +18,7 @@
  *   mi_gram_mi          _kernels.py:48-61 + gram.py:88-111 + engine.py:93-141
  *                                           (G11, closed-form counts, MI; fused)
  *   mi_generate_words   datagen.py:44-73    generate(GenSpec) stream, packed
+ *   mi_pack_bits        binmat.py:34-46,136-172  from_bits / from_rows (pack_bits), on the device
  *   mi_bmi_header,      io.py:92-116        read_bmi(path) (BMI1 container, io.py:1-16),
  *   mi_bmi_load                             payload streamed straight to the device
  * Extensions with no reference counterpart: mi_all_pairs_host_packed and
@@ -127,6 +128,13 @@ int mi_unpack_colsum_range(const uint64_t* d_words, int64_t n_rows, int64_t n_co
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
                int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
                int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
+/* binmat.from_bits / from_rows (binmat.py:34-46,136-172) on the device: a
+ * row-major uint8 0/1 matrix (n_rows x n_cols, row pitch ld_bits bytes) ->
+ * the words layout (n_cols x ceil(n_rows/64) uint64, padding bits zero).
+ * *d_bad (device int32, zeroed by the caller) gets bit 0 set if any byte is
+ * neither 0 nor 1 (from_rows's DomainError); the words are then not valid. */
+int mi_pack_bits(const uint8_t* d_bits, int64_t n_rows, int64_t n_cols, int64_t ld_bits, uint64_t* d_words,
+                 int32_t* d_bad, void* stream);
 /* ---- column order by column sum (configs with spread densities) ----
  * The fused epilogue's FP64-free table path needs each tile's column sums to
  * be clustered; computing in slots ordered by column sum makes that true for

@@ -637,6 +637,17 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
                         ld_out, d_tiles, n_tiles, nullptr, (cudaStream_t)stream);
 }
 
+int mi_pack_bits(const uint8_t* d_bits, int64_t n_rows, int64_t n_cols, int64_t ld_bits, uint64_t* d_words,
+                 int32_t* d_bad, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (ld_bits < n_cols) return fail(MI_ERR_DIMENSION, "ld_bits %lld < n_cols", (long long)ld_bits);
+    if (!d_bits || !d_words || !d_bad) return fail(MI_ERR_DOMAIN, "d_bits, d_words and d_bad are required");
+    MI_CUDA(launch_pack_bits(d_bits, n_rows, n_cols, ld_bits, d_words, reinterpret_cast<int*>(d_bad),
+                             (cudaStream_t)stream));
+    return MI_OK;
+}
+
 int mi_column_order(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int32_t* d_perm, int32_t* d_inv,
                     int32_t* d_spread, void* stream) {
     int rc = check_shape(n_rows, n_cols);

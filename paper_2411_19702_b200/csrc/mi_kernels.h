@@ -99,6 +99,11 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
                                 const uint8_t* block_mask, int tile, int64_t c_begin, int64_t c_end, int num_sms,
                                 cudaStream_t stream, const int32_t* perm = nullptr);
 
+// Device packing (pack.cu): row-major uint8 0/1 bits (n_rows x m, row pitch
+// ld bytes) -> words (m, ceil(n_rows / 64)) uint64; *bad |= 1 on a byte > 1.
+cudaError_t launch_pack_bits(const uint8_t* bits, int64_t n_rows, int64_t m, int64_t ld, uint64_t* words, int* bad,
+                             cudaStream_t stream);
+
 // Column order by column sum (order.cu): perm[s] = column in operand slot s
 // (ascending sum, ties by column index), inv[perm[s]] = s; spread (device
 // int[2], or nullptr) = (min, max) column sum.

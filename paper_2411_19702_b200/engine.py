@@ -147,6 +147,26 @@ class MIEngine:
         return t
 
     # ------------------------------------------------------------------ stages
+    def pack_bits(self, bits_dev: torch.Tensor, check: bool = True) -> torch.Tensor:
+        """binmat.from_bits / from_rows on the device (mi_pack_bits): a
+        row-major (N, m) uint8 / bool 0/1 tensor -> words (m, nw) int64.  With
+        ``check`` a non-binary byte raises DomainError like the reference's
+        from_rows (one 4-byte read back)."""
+        if bits_dev.device != self.device or bits_dev.dim() != 2 or bits_dev.element_size() != 1 \
+                or bits_dev.stride(1) != 1:
+            raise DimensionError("bits must be a row-major (N, m) uint8/bool tensor on the engine's device")
+        n, m = int(bits_dev.shape[0]), int(bits_dev.shape[1])
+        if n < 1 or m < 1:
+            raise DimensionError("matrix must have at least one row and one column")
+        words = torch.empty((m, n_words(n)), dtype=torch.int64, device=self.device)
+        bad = torch.zeros((1,), dtype=torch.int32, device=self.device)
+        nat.check(nat.lib().mi_pack_bits(bits_dev.data_ptr(), n, m, bits_dev.stride(0), words.data_ptr(),
+                                         bad.data_ptr(), _stream_ptr(self.device)),
+                  "mi_pack_bits")
+        if check and int(bad.item()) != 0:
+            raise DomainError("values must be 0 or 1")
+        return words
+
     def upload(self, words: np.ndarray) -> torch.Tensor:
         """Host words (m, nw) uint64 -> device tensor (int64 storage, same bits)."""
         host = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))

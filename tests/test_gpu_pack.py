@@ -1,0 +1,49 @@
+"""Device packing (mi_pack_bits, MIEngine.pack_bits): the reference's
+from_bits / from_rows layout bit for bit, at ragged shapes and pitches, with
+from_rows's rejection of non-binary values (binmat.py:34-46,136-172)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (63, 5), (64, 128), (65, 129), (255, 300), (256, 127), (1000, 700),
+                                 (4097, 1300), (20_000, 257)])
+def test_pack_matches_reference_layout(engine, n, m):
+    rng = np.random.default_rng(n + 31 * m)
+    bits = (rng.random((n, m)) < rng.uniform(0, 1)).astype(np.uint8)
+    words = engine.pack_bits(torch.from_numpy(bits).to(engine.device)).cpu().numpy().view(np.uint64)
+    assert np.array_equal(words, O.pack_bits(bits))
+    # a pitched view (row stride > m) and bool input give the same words
+    wide = np.zeros((n, m + 13), dtype=np.uint8)
+    wide[:, :m] = bits
+    view = torch.from_numpy(wide).to(engine.device)[:, :m]
+    assert np.array_equal(engine.pack_bits(view).cpu().numpy().view(np.uint64), words)
+    as_bool = torch.from_numpy(bits.astype(bool)).to(engine.device)
+    assert np.array_equal(engine.pack_bits(as_bool).cpu().numpy().view(np.uint64), words)
+
+
+def test_pack_then_mi_end_to_end(engine):
+    rng = np.random.default_rng(5)
+    n, m = 3000, 600
+    bits = (rng.random((n, m)) < 0.3).astype(np.uint8)
+    w = engine.pack_bits(torch.from_numpy(bits).to(engine.device))
+    mi = engine.all_pairs_device(w, n, m).cpu().numpy()
+    assert float(np.max(np.abs(mi - O.c_mi_all_pairs(O.pack_bits(bits), n)))) < 1e-12
+
+
+def test_pack_rejects_non_binary(engine):
+    from paper_2411_19702_b200.errors import DimensionError, DomainError
+
+    bits = np.zeros((300, 200), dtype=np.uint8)
+    bits[123, 45] = 2
+    with pytest.raises(DomainError):
+        engine.pack_bits(torch.from_numpy(bits).to(engine.device))
+    with pytest.raises(DimensionError):
+        engine.pack_bits(torch.zeros((4, 4), dtype=torch.int32, device=engine.device))
