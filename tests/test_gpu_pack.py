@@ -47,3 +47,25 @@ def test_pack_rejects_non_binary(engine):
         engine.pack_bits(torch.from_numpy(bits).to(engine.device))
     with pytest.raises(DimensionError):
         engine.pack_bits(torch.zeros((4, 4), dtype=torch.int32, device=engine.device))
+
+
+def test_engine_from_bits_host(engine):
+    from paper_2411_19702_b200.binmat import from_bits
+    from paper_2411_19702_b200.errors import DomainError
+
+    rng = np.random.default_rng(8)
+    bits = (rng.random((5000, 777)) < 0.4).astype(np.uint8)
+    got = engine.from_bits(bits)
+    want = from_bits(bits)
+    assert got.n_rows == want.n_rows and got.n_cols == want.n_cols
+    assert np.array_equal(got.words, want.words)
+    assert np.array_equal(engine.from_bits(bits.astype(np.int64)).words, want.words)
+    assert np.array_equal(engine.from_bits(bits.astype(bool)).words, want.words)
+    bad = bits.astype(np.int64)
+    bad[3, 3] = 5
+    with pytest.raises(DomainError):
+        engine.from_bits(bad)
+    bad8 = bits.copy()
+    bad8[10, 20] = 2
+    with pytest.raises(DomainError):
+        engine.from_bits(bad8)
