@@ -410,6 +410,7 @@ struct Workspace {
     void* colstat = nullptr; size_t colstat_cap = 0;
     void* tiles = nullptr; size_t tiles_cap = 0;
     void* out = nullptr; size_t out_cap = 0;
+    void* h_stage = nullptr; size_t h_stage_cap = 0;  // pinned staging of pageable host words
     cudaStream_t copy_stream = nullptr;   // D2H of finished row bands
     cudaEvent_t copy_ev[2] = {nullptr, nullptr};  // the last two D2H copies
     cudaEvent_t stage_ev[kMaxIngestStages] = {};  // staged path: stage g's tiles are stored
@@ -446,6 +447,8 @@ void release(Workspace& w) {
     for (auto& e : w.stage_ev)
         if (e) cudaEventDestroy(e), e = nullptr;
     if (w.row_done_h) cudaFreeHost(w.row_done_h), w.row_done_h = nullptr, w.row_done_d = nullptr;
+    if (w.h_stage) cudaFreeHost(w.h_stage), w.h_stage = nullptr;
+    w.h_stage_cap = 0;
     w.row_done_cap = 0;
     w.device = -1;
     cudaSetDevice(prev);
@@ -815,6 +818,37 @@ int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_
                                true);
 }
 
+// True when h points into page-locked (or registered / managed) host memory
+// that the copy engines can read directly.
+bool host_is_pinned(const void* h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// memcpy with up to `threads` host threads (pageable -> pinned staging): one
+// thread reaches ~10 GB/s, well short of the link's ~55.
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    const size_t min_chunk = (size_t)4 << 20;
+    int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
+    if (t <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t chunk = (bytes + t - 1) / t;
+    for (int i = 0; i < t; ++i) {
+        const size_t o = (size_t)i * chunk;
+        if (o >= bytes) break;
+        const size_t n = std::min(chunk, bytes - o);
+        pool.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, n); });
+    }
+    for (auto& th : pool) th.join();
+}
+
 // Staged ingest -> compute -> egress (full-matrix output): the column blocks
 // are cut into S groups; group g's words go H2D and are unpacked, then the
 // tiles whose larger block falls in group g run (all their operands are
@@ -875,6 +909,25 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
     MI_CUDA(launch_unpack_prep(n_rows, m_pad, cs, xl, br, fixr_ptr(ws.colstat, n_rows, n_cols), info.num_sms,
                                ws.stream));
     const size_t pitch = (size_t)n_cols * esz;
+    // Pageable words (the drop-in's numpy arrays) copy at ~10 GB/s through the
+    // driver's bounce buffer, one stage after another, which starved the
+    // pipeline (config 3: 14 ms of upload).  Stage them into a pinned buffer
+    // with host threads instead, group by group, so each group's H2D runs at
+    // link speed while the next group is being copied.
+    const uint64_t* src_words = h_words;
+    const bool stage_host = !host_is_pinned(h_words);
+    if (stage_host) {
+        const size_t need = (size_t)(n_cols * nw * 8);
+        if (ws.h_stage_cap < need) {
+            if (ws.h_stage) cudaFreeHost(ws.h_stage);
+            ws.h_stage = nullptr;
+            ws.h_stage_cap = 0;
+            MI_CUDA(cudaHostAlloc(&ws.h_stage, need, cudaHostAllocDefault));
+            ws.h_stage_cap = need;
+        }
+        src_words = (const uint64_t*)ws.h_stage;
+    }
+    const int copy_threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
     // MI_B200_TIMELINE=1: per-stage event timeline on stderr (experiments only)
     const bool tl_on = env_int("MI_B200_TIMELINE", 0) != 0;
     std::vector<cudaEvent_t> tl;
@@ -888,7 +941,10 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
     mark(ws.stream);
     for (int g = 0; g < S; ++g) {
         const int64_t c0 = std::min<int64_t>(blk[g] * tile, n_cols), c1 = std::min<int64_t>(blk[g + 1] * tile, n_cols);
-        MI_CUDA(cudaMemcpyAsync((uint64_t*)ws.words + c0 * nw, h_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
+        if (stage_host)  // (the previous groups' H2D copies read other parts of the staging buffer)
+            parallel_memcpy((uint64_t*)ws.h_stage + c0 * nw, h_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
+                            copy_threads);
+        MI_CUDA(cudaMemcpyAsync((uint64_t*)ws.words + c0 * nw, src_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
                                 cudaMemcpyHostToDevice, ws.stream));
         mark(ws.stream);  // H2D g done
         const int64_t u1 = g == S - 1 ? m_pad : blk[g + 1] * tile;
