@@ -153,14 +153,17 @@ class MIEngine:
         ``check`` a non-binary byte raises DomainError like the reference's
         from_rows (one 4-byte read back)."""
         if bits_dev.device != self.device or bits_dev.dim() != 2 or bits_dev.element_size() != 1 \
-                or bits_dev.stride(1) != 1:
-            raise DimensionError("bits must be a row-major (N, m) uint8/bool tensor on the engine's device")
+                or bits_dev.dtype not in (torch.uint8, torch.bool, torch.int8):
+            raise DimensionError("bits must be an (N, m) uint8/bool tensor on the engine's device")
         n, m = int(bits_dev.shape[0]), int(bits_dev.shape[1])
         if n < 1 or m < 1:
             raise DimensionError("matrix must have at least one row and one column")
+        if bits_dev.stride(1) != 1 or (n > 1 and bits_dev.stride(0) < m):
+            bits_dev = bits_dev.contiguous()  # the kernel reads rows with unit column stride
+        ld = bits_dev.stride(0) if n > 1 else m
         words = torch.empty((m, n_words(n)), dtype=torch.int64, device=self.device)
         bad = torch.zeros((1,), dtype=torch.int32, device=self.device)
-        nat.check(nat.lib().mi_pack_bits(bits_dev.data_ptr(), n, m, bits_dev.stride(0), words.data_ptr(),
+        nat.check(nat.lib().mi_pack_bits(bits_dev.data_ptr(), n, m, ld, words.data_ptr(),
                                          bad.data_ptr(), _stream_ptr(self.device)),
                   "mi_pack_bits")
         if check and int(bad.item()) != 0:

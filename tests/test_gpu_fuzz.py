@@ -57,3 +57,40 @@ def test_fuzz_case(engine, k):
     tol = 1e-12 if dtype == "float64" else 1e-6
     err = float(np.max(np.abs(mi.astype(np.float64) - ref)))
     assert err < tol, (n, m, mode, diag, dtype, knobs, err)
+
+
+@pytest.mark.parametrize("k", range(24))
+def test_fuzz_new_paths(engine, k):
+    """The same random cases through the column-sum order, the staged host
+    path (random group count, pageable or pinned words) and the device packer:
+    counts bit-exact, MI within tolerance, host path bit-identical to the
+    device path."""
+    from paper_2411_19702_b200 import EngineConfig
+    from paper_2411_19702_b200 import _native as nat
+
+    n, m, words, mode, diag, dtype, _ = _case(100 + k)
+    rng = np.random.default_rng(5000 + k)
+    cfg = EngineConfig(mode=mode, epsilon=1e-10, include_diagonal=diag)
+    dt = getattr(torch, dtype)
+    tol = 1e-12 if dtype == "float64" else 1e-6
+    ref = O.c_mi_all_pairs(words, n, mode=mode, epsilon=1e-10, include_diagonal=diag)
+    bits = O.unpack_bits(words, n)
+    dev = engine.pack_bits(torch.from_numpy(bits).to(engine.device))
+    assert np.array_equal(dev.cpu().numpy().view(np.uint64), words)
+    # column-sum order
+    got = engine.all_pairs_device(dev, n, m, cfg, dt, order="colsum").double().cpu().numpy()
+    assert np.array_equal(got, got.T)
+    assert float(np.max(np.abs(got - ref))) < tol, (n, m, "colsum")
+    prep = engine.prepare(dev, n, m, order="colsum")
+    g = engine.compute(prep, None, torch.int32).cpu().numpy().astype(np.int64)
+    assert np.array_equal(g, O.c_gram_ones(words))
+    # staged host path vs the device path
+    natural = engine.all_pairs_device(dev, n, m, cfg, dt).cpu().numpy()
+    old = nat.get_tuning("ingest")
+    try:
+        nat.set_tuning(ingest=int(rng.integers(0, 9)))
+        src = torch.from_numpy(words.view(np.int64)).pin_memory() if rng.random() < 0.5 else words
+        host = engine.all_pairs_host(src, n, m, cfg, dt).numpy()
+    finally:
+        nat.set_tuning(ingest=old)
+    assert np.array_equal(host, natural)

@@ -49,6 +49,17 @@ def test_pack_rejects_non_binary(engine):
         engine.pack_bits(torch.zeros((4, 4), dtype=torch.int32, device=engine.device))
 
 
+def test_pack_transposed_and_single_row_views(engine):
+    rng = np.random.default_rng(12)
+    bits = (rng.random((300, 1)) < 0.5).astype(np.uint8)
+    for arr in (bits, bits.T, np.asfortranarray((rng.random((50, 70)) < 0.5).astype(np.uint8))):
+        t = torch.from_numpy(np.asarray(arr)).to(engine.device)
+        if arr.shape[1] > 1:
+            t = torch.from_numpy(np.ascontiguousarray(arr).T.copy()).to(engine.device).T  # column-major view
+        w = engine.pack_bits(t).cpu().numpy().view(np.uint64)
+        assert np.array_equal(w, O.pack_bits(np.ascontiguousarray(t.cpu().numpy())))
+
+
 def test_engine_from_bits_host(engine):
     from paper_2411_19702_b200.binmat import from_bits
     from paper_2411_19702_b200.errors import DomainError
