@@ -370,3 +370,27 @@ def test_serpentine_k_order_is_bit_identical(engine):
     assert np.array_equal(res[0][0], res[1][0])
     assert np.array_equal(res[0][1], res[1][1])
     assert np.array_equal(res[1][0], O.c_gram_ones(words))
+
+
+def test_invariants_like_the_reference(engine):
+    """test_engine.py:157-219's invariant suite through the GPU path: row
+    permutation leaves the matrix bit-identical (the counts are identical),
+    complementing a column or duplicating every row changes MI by < 1e-12,
+    0 <= MI(i, j) <= min(H_i, H_j), epsilon mode within 1e-6 of exact."""
+    rng = np.random.default_rng(2024)
+    n, m = 3000, 700
+    dens = rng.uniform(0.05, 0.95, m)
+    bits = (rng.random((n, m)) < dens[None, :]).astype(np.uint8)
+    base = gpu_mi(engine, O.pack_bits(bits), n)
+    perm = rng.permutation(n)
+    assert np.array_equal(gpu_mi(engine, O.pack_bits(bits[perm]), n), base)
+    comp = bits.copy()
+    comp[:, 5] = 1 - comp[:, 5]
+    assert float(np.max(np.abs(gpu_mi(engine, O.pack_bits(comp), n) - base))) < 1e-12
+    dup = np.concatenate([bits, bits], axis=0)
+    assert float(np.max(np.abs(gpu_mi(engine, O.pack_bits(dup), 2 * n) - base))) < 1e-12
+    h = np.diagonal(base)
+    assert base.min() >= -1e-12
+    assert float(np.max(base - np.minimum(h[:, None], h[None, :]))) <= 1e-12
+    eps = gpu_mi(engine, O.pack_bits(bits), n, cfg_of("epsilon", 1e-12))
+    assert float(np.max(np.abs(eps - base))) <= 1e-6
