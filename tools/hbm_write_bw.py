@@ -1,4 +1,8 @@
-"""Write-only and copy HBM bandwidth on this box (torch fill_/copy_, 1 GiB)."""
+"""Write-only and copy HBM bandwidth on this box (torch fill_/copy_, 1 GiB).
+
+Caveat: torch's fill_ kernel reports ~3.9 TB/s of writes, well below what the
+HBM takes; hand-written store kernels and cudaMemset reach 7.0-7.3 TB/s
+(tools/micro/write_bw.cu), which is the write roofline DESIGN.md uses."""
 import torch
 x = torch.empty(1 << 30, dtype=torch.int8, device="cuda")
 y = torch.empty(1 << 30, dtype=torch.int8, device="cuda")
