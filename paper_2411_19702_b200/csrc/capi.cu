@@ -14,6 +14,7 @@
 #include <chrono>
 #include <mutex>
 #include <thread>
+#include <condition_variable>
 #include <vector>
 
 #include "../../include/mimatrix_b200.h"
@@ -830,23 +831,64 @@ bool host_is_pinned(const void* h) {
 }
 
 // memcpy with up to `threads` host threads (pageable -> pinned staging): one
-// thread reaches ~10 GB/s, well short of the link's ~55.
+// thread reaches ~10 GB/s, well short of the link's ~55.  The workers are a
+// small persistent pool (created on first use, never torn down: spawning 8
+// threads per group cost ~1 ms a call); calls are serialised by g_ws_mu.
+struct CopyPool {
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::vector<std::thread> workers;
+    struct Job { char* dst; const char* src; size_t n; };
+    std::vector<Job> jobs;
+    size_t next = 0, pending = 0;
+    void ensure(int n) {
+        while ((int)workers.size() < n) {
+            workers.emplace_back([this] {
+                for (;;) {
+                    Job j;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [this] { return next < jobs.size(); });
+                        j = jobs[next++];
+                    }
+                    memcpy(j.dst, j.src, j.n);
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (--pending == 0) done_cv.notify_all();
+                }
+            });
+            workers.back().detach();
+        }
+    }
+};
+CopyPool& copy_pool() {
+    static CopyPool* p = new CopyPool();  // leaked on purpose: detached workers outlive static destruction
+    return *p;
+}
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
     const size_t min_chunk = (size_t)4 << 20;
-    int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
+    const int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
     if (t <= 1) {
         memcpy(dst, src, bytes);
         return;
     }
-    std::vector<std::thread> pool;
+    CopyPool& pool = copy_pool();
+    pool.ensure(t);
     const size_t chunk = (bytes + t - 1) / t;
-    for (int i = 0; i < t; ++i) {
-        const size_t o = (size_t)i * chunk;
-        if (o >= bytes) break;
-        const size_t n = std::min(chunk, bytes - o);
-        pool.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, n); });
+    {
+        std::lock_guard<std::mutex> lk(pool.mu);
+        pool.jobs.clear();
+        pool.next = 0;
+        for (int i = 0; i < t; ++i) {
+            const size_t o = (size_t)i * chunk;
+            if (o >= bytes) break;
+            pool.jobs.push_back({(char*)dst + o, (const char*)src + o, std::min(chunk, bytes - o)});
+        }
+        pool.pending = pool.jobs.size();
     }
-    for (auto& th : pool) th.join();
+    pool.cv.notify_all();
+    std::unique_lock<std::mutex> lk(pool.mu);
+    pool.done_cv.wait(lk, [&] { return pool.pending == 0; });
 }
 
 // Staged ingest -> compute -> egress (full-matrix output): the column blocks
