@@ -298,7 +298,10 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
     const dim3 grid((unsigned)((c_end - c_begin + kUnpackCols - 1) / kUnpackCols), (unsigned)chunks);
     if (fp4) {
         const int64_t nkb = ld / 128;
-        constexpr int KB = 32, UNR = 8;  // tools/unpack_bench.py sweep (r01h): best across configs 3-5
+        // tools/unpack_bench.py sweeps (r01h, r01m): 32 k-blocks per block and 16
+        // loads in flight per thread were best across configs 3-5 (the kernel
+        // is memory-latency bound at 50% occupancy: ncu long-scoreboard stalls)
+        constexpr int KB = 32, UNR = 16;
         const dim3 g2((unsigned)((c_end - c_begin + kDirectCols - 1) / kDirectCols), (unsigned)((nkb + KB - 1) / KB));
         if (g2.y > 65535) return cudaErrorInvalidValue;
         unpack_fp4_direct_kernel<KB, UNR><<<g2, 256, 0, stream>>>(words, m, nw, x, nkb, m_pad, colstat, block_mask,
