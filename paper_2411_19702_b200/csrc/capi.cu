@@ -456,6 +456,107 @@ void release(Workspace& w) {
 }
 
 // words (host) -> X, colsum on the device; shared by the host entry points.
+// True when h points into page-locked (or registered / managed) host memory
+// that the copy engines can read directly.
+bool host_is_pinned(const void* h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// memcpy with up to `threads` host threads (pageable -> pinned staging): one
+// thread reaches ~10 GB/s, well short of the link's ~55.  The workers are a
+// small persistent pool (created on first use, never torn down: spawning 8
+// threads per group cost ~1 ms a call); calls are serialised by g_ws_mu.
+struct CopyPool {
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::vector<std::thread> workers;
+    struct Job { char* dst; const char* src; size_t n; };
+    std::vector<Job> jobs;
+    size_t next = 0, pending = 0;
+    void ensure(int n) {
+        while ((int)workers.size() < n) {
+            workers.emplace_back([this] {
+                for (;;) {
+                    Job j;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [this] { return next < jobs.size(); });
+                        j = jobs[next++];
+                    }
+                    memcpy(j.dst, j.src, j.n);
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (--pending == 0) done_cv.notify_all();
+                }
+            });
+            workers.back().detach();
+        }
+    }
+};
+CopyPool& copy_pool() {
+    static CopyPool* p = new CopyPool();  // leaked on purpose: detached workers outlive static destruction
+    return *p;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    const size_t min_chunk = (size_t)4 << 20;
+    const int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
+    if (t <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    CopyPool& pool = copy_pool();
+    pool.ensure(t);
+    const size_t chunk = (bytes + t - 1) / t;
+    {
+        std::lock_guard<std::mutex> lk(pool.mu);
+        pool.jobs.clear();
+        pool.next = 0;
+        for (int i = 0; i < t; ++i) {
+            const size_t o = (size_t)i * chunk;
+            if (o >= bytes) break;
+            pool.jobs.push_back({(char*)dst + o, (const char*)src + o, std::min(chunk, bytes - o)});
+        }
+        pool.pending = pool.jobs.size();
+    }
+    pool.cv.notify_all();
+    std::unique_lock<std::mutex> lk(pool.mu);
+    pool.done_cv.wait(lk, [&] { return pool.pending == 0; });
+}
+
+// H2D of host words into ws.words on ws.stream.  Pageable words (numpy
+// arrays) go through the cached pinned staging buffer in 4 column chunks:
+// host threads copy chunk k while the copy engine moves chunk k - 1 (the
+// driver's own pageable path runs at ~10 GB/s).
+int upload_words(Workspace& ws, const uint64_t* h_words, int64_t n_cols, int64_t nw) {
+    const size_t bytes = (size_t)(n_cols * nw * 8);
+    if (host_is_pinned(h_words)) {
+        MI_CUDA(cudaMemcpyAsync(ws.words, h_words, bytes, cudaMemcpyHostToDevice, ws.stream));
+        return MI_OK;
+    }
+    if (ws.h_stage_cap < bytes) {
+        if (ws.h_stage) cudaFreeHost(ws.h_stage);
+        ws.h_stage = nullptr;
+        ws.h_stage_cap = 0;
+        MI_CUDA(cudaHostAlloc(&ws.h_stage, bytes, cudaHostAllocDefault));
+        ws.h_stage_cap = bytes;
+    }
+    const int threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    const int64_t chunks = n_cols >= 4 ? 4 : 1;
+    for (int64_t k = 0; k < chunks; ++k) {
+        const int64_t c0 = n_cols * k / chunks, c1 = n_cols * (k + 1) / chunks;
+        const size_t off = (size_t)(c0 * nw * 8), len = (size_t)((c1 - c0) * nw * 8);
+        parallel_memcpy((char*)ws.h_stage + off, (const char*)h_words + off, len, threads);
+        MI_CUDA(cudaMemcpyAsync((char*)ws.words + off, (char*)ws.h_stage + off, len, cudaMemcpyHostToDevice,
+                                ws.stream));
+    }
+    return MI_OK;
+}
+
 int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int64_t* ld_out,
                  int64_t* m_pad_out, const DevInfo& info) {
     const int64_t nw = (n_rows + 63) / 64;
@@ -466,7 +567,7 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
     if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
     if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
-    MI_CUDA(cudaMemcpyAsync(ws.words, h_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
+    if ((rc = upload_words(ws, h_words, n_cols, nw))) return rc;
     MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
                                  (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
                                  blkrange_ptr(ws.colstat, n_rows, n_cols), fixr_ptr(ws.colstat, n_rows, n_cols),
@@ -817,78 +918,6 @@ int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_
                              int include_diagonal, int out_kind, void* h_out, int device) {
     return all_pairs_host_impl(h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out, device,
                                true);
-}
-
-// True when h points into page-locked (or registered / managed) host memory
-// that the copy engines can read directly.
-bool host_is_pinned(const void* h) {
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
-}
-
-// memcpy with up to `threads` host threads (pageable -> pinned staging): one
-// thread reaches ~10 GB/s, well short of the link's ~55.  The workers are a
-// small persistent pool (created on first use, never torn down: spawning 8
-// threads per group cost ~1 ms a call); calls are serialised by g_ws_mu.
-struct CopyPool {
-    std::mutex mu;
-    std::condition_variable cv, done_cv;
-    std::vector<std::thread> workers;
-    struct Job { char* dst; const char* src; size_t n; };
-    std::vector<Job> jobs;
-    size_t next = 0, pending = 0;
-    void ensure(int n) {
-        while ((int)workers.size() < n) {
-            workers.emplace_back([this] {
-                for (;;) {
-                    Job j;
-                    {
-                        std::unique_lock<std::mutex> lk(mu);
-                        cv.wait(lk, [this] { return next < jobs.size(); });
-                        j = jobs[next++];
-                    }
-                    memcpy(j.dst, j.src, j.n);
-                    std::lock_guard<std::mutex> lk(mu);
-                    if (--pending == 0) done_cv.notify_all();
-                }
-            });
-            workers.back().detach();
-        }
-    }
-};
-CopyPool& copy_pool() {
-    static CopyPool* p = new CopyPool();  // leaked on purpose: detached workers outlive static destruction
-    return *p;
-}
-
-void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
-    const size_t min_chunk = (size_t)4 << 20;
-    const int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
-    if (t <= 1) {
-        memcpy(dst, src, bytes);
-        return;
-    }
-    CopyPool& pool = copy_pool();
-    pool.ensure(t);
-    const size_t chunk = (bytes + t - 1) / t;
-    {
-        std::lock_guard<std::mutex> lk(pool.mu);
-        pool.jobs.clear();
-        pool.next = 0;
-        for (int i = 0; i < t; ++i) {
-            const size_t o = (size_t)i * chunk;
-            if (o >= bytes) break;
-            pool.jobs.push_back({(char*)dst + o, (const char*)src + o, std::min(chunk, bytes - o)});
-        }
-        pool.pending = pool.jobs.size();
-    }
-    pool.cv.notify_all();
-    std::unique_lock<std::mutex> lk(pool.mu);
-    pool.done_cv.wait(lk, [&] { return pool.pending == 0; });
 }
 
 // Staged ingest -> compute -> egress (full-matrix output): the column blocks
