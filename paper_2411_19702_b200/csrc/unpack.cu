@@ -11,9 +11,10 @@
 // The same pass produces v[c] = popcount of column c, i.e. the reference's
 // column_sums (binmat.py:175-177), which the fused epilogue needs.
 //
-// HBM-bound: reads 8*m*nw bytes, writes m_pad*N_pad bytes.  Blocks of 32
-// columns transpose through shared memory so that both the word reads and the
-// byte writes are long contiguous runs (below).
+// HBM-bound: reads 8*m*nw bytes, writes m_pad*N_pad (int8) or m_pad*N_pad/2
+// (e2m1) bytes.  No shared memory: each thread expands whole words of one
+// column straight from its loads, and a warp's stores form one contiguous run
+// of X (unpack_direct_kernel, below).
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -88,37 +89,8 @@ __device__ __forceinline__ void write_colstat(int64_t c, uint32_t cnt, int64_t n
     }
 }
 
-// Expansion: block (g, k) owns 32 columns c0 = 32 g .. c0 + 31 and K chunk k
-// (kUnpackTiles tiles of 64 words).  Each tile's 32 x 512 bytes of words are
-// staged in shared memory by cp.async (double-buffered: tile i + 1 loads while
-// tile i expands); then every warp expands whole k-blocks: lane l owns column
-// c0 + l, turns its 2 words into 128 bytes (four STG.256), and the warp's
-// stores fill one contiguous 4 KB run of X (the group's 32 rows of one
-// k-block).  Ones are counted on the fly into ColStat::vi.
+// Column ranges of the staged launches start on multiples of 32.
 constexpr int kUnpackCols = 32;
-constexpr int kUnpackWords = 64;                // words per column per K tile (= 32 k-blocks)
-constexpr int kUnpackPitch = kUnpackWords + 1;  // smem row pitch in words (2-way banks at most)
-constexpr int kUnpackTiles = 4;                 // tiles per block (K chunk = 256 words)
-
-__device__ __forceinline__ void store_row128(int8_t* dst, uint64_t w0, uint64_t w1) {
-    uint32_t q[32];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        q[k] = spread4((uint32_t)(w0 >> (4 * k)) & 0xFu);
-        q[16 + k] = spread4((uint32_t)(w1 >> (4 * k)) & 0xFu);
-    }
-#pragma unroll
-    for (int h = 0; h < 4; ++h)
-        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 32 * h),
-                     "r"(q[8 * h + 0]), "r"(q[8 * h + 1]), "r"(q[8 * h + 2]), "r"(q[8 * h + 3]), "r"(q[8 * h + 4]),
-                     "r"(q[8 * h + 5]), "r"(q[8 * h + 6]), "r"(q[8 * h + 7])
-                     : "memory");
-}
-
-__device__ __forceinline__ void cp_async8(uint64_t* smem_dst, const uint64_t* src, bool valid) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
-}
 
 // 64 bits -> 32 bytes of e2m1 nibbles (row 2j in the low nibble of byte j,
 // row 2j + 1 in the high one; 1.0 = 0b0010), one STG.256.  fp4x8 moves bit k
@@ -145,101 +117,53 @@ __device__ __forceinline__ void store_fp4_word(int8_t* dst, uint64_t w) {
                  : "memory");
 }
 
-template <bool FP4>
-__global__ void __launch_bounds__(256)
-unpack_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x, int64_t ld,
-              int64_t m_pad, ColStat* __restrict__ colstat, const uint8_t* __restrict__ block_mask, int tile_cols,
-              const int32_t* __restrict__ perm, int64_t col_base) {
-    const int64_t c0 = col_base + (int64_t)blockIdx.x * kUnpackCols;  // first column of this block
-    if (block_mask && !block_mask[c0 / tile_cols]) return;  // not this rank's block
-    __shared__ __align__(16) uint64_t tile[2][kUnpackCols * kUnpackPitch];
-    constexpr int WPK = FP4 ? 4 : 2;           // words per 128-byte k-block row
-    constexpr int KBT = kUnpackWords / WPK;    // k-blocks per tile
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const int64_t nkb = ld / 128;
-    const int64_t wpad = nkb * WPK;            // words per padded column
-    const int64_t kb_stride = m_pad * 128;
-    const int ld_col = t >> 3;     // loader: column of the group
-    const int ld_sub = t & 7;      // loader: 8 words of the tile row
-    const int64_t lc = c0 + ld_col;
-    const bool lreal = lc < m;
-    // slot lc holds column perm[lc] (column order by column sum, order.cu) or column lc
-    const uint64_t* __restrict__ src = words + (lreal ? (perm ? (int64_t)__ldg(perm + lc) : lc) : 0) * nw;
-    const int64_t wbeg = (int64_t)blockIdx.y * kUnpackTiles * kUnpackWords;
-    int ntiles = (int)((wpad - wbeg + kUnpackWords - 1) / kUnpackWords);
-    if (ntiles > kUnpackTiles) ntiles = kUnpackTiles;
-    auto issue = [&](int i) {
-        uint64_t* dstrow = &tile[i & 1][ld_col * kUnpackPitch + ld_sub * 8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int64_t w = wbeg + (int64_t)i * kUnpackWords + ld_sub * 8 + k;
-            const bool ok = lreal && w < nw;
-            cp_async8(dstrow + k, src + (ok ? w : 0), ok);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    uint32_t cnt = 0;
-    issue(0);
-    for (int i = 0; i < ntiles; ++i) {
-        if (i + 1 < ntiles) {
-            issue(i + 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
-        const uint64_t* buf = tile[i & 1];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) cnt += __popcll(buf[ld_col * kUnpackPitch + ld_sub * 8 + k]);
-        const int64_t kb0 = (wbeg + (int64_t)i * kUnpackWords) / WPK;
-#pragma unroll
-        for (int kk = 0; kk < KBT; kk += 8) {
-            const int kbl = kk + warp;
-            if (kb0 + kbl < nkb) {
-                int8_t* dst = x + (kb0 + kbl) * kb_stride + (c0 + lane) * 128;
-                const uint64_t* wsrc = buf + lane * kUnpackPitch + WPK * kbl;
-                if constexpr (FP4) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) store_fp4_word(dst + 32 * q, wsrc[q]);
-                } else {
-                    store_row128(dst, wsrc[0], wsrc[1]);
-                }
-            }
-        }
-        __syncthreads();  // buffer i & 1 is reloaded by issue(i + 2)
-    }
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
-    if (ld_sub == 0 && cnt) atomicAdd(&colstat[lc].vi, (int)cnt);
-}
-
-// e2m1 expansion without shared memory.  Thread (c, j) -- c one of the
+// Expansion without shared memory (e2m1 case described; int8 below).  Thread (c, j) -- c one of the
 // block's 64 columns (8 per warp), j = lane & 3 the word within a k-block --
 // loads word 4 kb + j of column c (8 bytes: a column's four lanes read one
 // full 32-byte sector) and stores its 32 bytes of nibbles with one STG.256;
 // the warp's 8 columns x 128 bytes are one contiguous 1 KB run of X.  kUnr
 // k-blocks are loaded before any is expanded, so every thread keeps kUnr
-// loads in flight.  (The staged kernel above spends its time in the L1/shared
-// pipeline -- cp.async of 8-byte pieces, then shared-memory reads -- at ~2.7
-// TB/s of writes; this box writes HBM at ~7 TB/s, tools/micro/write_bw.cu.)
-constexpr int kDirectCols = 64;  // columns per block (8 warps x 8)
-template <int kDirectKb, int kUnr>
+// loads in flight.  (The cp.async-staged kernel this replaced spent its time
+// in the L1/shared pipeline at ~2.7 TB/s of writes; this box writes HBM at
+// ~7 TB/s, tools/micro/write_bw.cu.)
+// 64 bits -> 64 bytes of 0/1 (int8 operand): two STG.256.
+__device__ __forceinline__ void store_int8_word(int8_t* dst, uint64_t w) {
+    uint32_t q[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) q[k] = spread4((uint32_t)(w >> (4 * k)) & 0xFu);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 32 * h),
+                     "r"(q[8 * h + 0]), "r"(q[8 * h + 1]), "r"(q[8 * h + 2]), "r"(q[8 * h + 3]), "r"(q[8 * h + 4]),
+                     "r"(q[8 * h + 5]), "r"(q[8 * h + 6]), "r"(q[8 * h + 7])
+                     : "memory");
+}
+
+// FP4 = false: the same for the int8 operand (a 128-byte k-block row holds
+// 2 words; each word becomes 64 bytes of 0/1, two STG.256), 16 columns per
+// warp, so a warp's stores are one contiguous 2 KB run.
+template <bool FP4>
+struct DirectShape {
+    static constexpr int WPK = FP4 ? 4 : 2;          // words per 128-byte k-block row
+    static constexpr int COLS_PER_WARP = 32 / WPK;   // 8 (e2m1) or 16 (int8)
+    static constexpr int COLS = 8 * COLS_PER_WARP;   // per 256-thread block
+};
+template <bool FP4, int kDirectKb, int kUnr>
 __global__ void __launch_bounds__(256)
-unpack_fp4_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x,
-                         int64_t nkb, int64_t m_pad, ColStat* __restrict__ colstat,
-                         const uint8_t* __restrict__ block_mask, int tile_cols, const int32_t* __restrict__ perm,
-                         int64_t col_base, int64_t col_end) {
+unpack_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, int8_t* __restrict__ x,
+                     int64_t nkb, int64_t m_pad, ColStat* __restrict__ colstat,
+                     const uint8_t* __restrict__ block_mask, int tile_cols, const int32_t* __restrict__ perm,
+                     int64_t col_base, int64_t col_end) {
+    using D = DirectShape<FP4>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = lane & 3;
-    const int64_t c = col_base + (int64_t)blockIdx.x * kDirectCols + warp * 8 + (lane >> 2);
+    const int j = lane % D::WPK;
+    const int64_t c = col_base + (int64_t)blockIdx.x * D::COLS + warp * D::COLS_PER_WARP + lane / D::WPK;
     // no early return: the count reduction below shuffles across the warp
     const bool active = c < col_end && (!block_mask || block_mask[c / tile_cols]);
     const bool real = active && c < m;
     const uint64_t* __restrict__ src = words + (real ? (perm ? (int64_t)__ldg(perm + c) : c) : 0) * nw;
     const int64_t kb_stride = m_pad * 128;
-    int8_t* const xc = x + c * 128 + j * 32;
+    int8_t* const xc = x + c * 128 + j * (128 / D::WPK);
     const int64_t kb0 = (int64_t)blockIdx.y * kDirectKb;
     const int64_t kb1 = kb0 + kDirectKb < nkb ? kb0 + kDirectKb : nkb;
     uint32_t cnt = 0;
@@ -247,7 +171,7 @@ unpack_fp4_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t 
         uint64_t wv[kUnr];
 #pragma unroll
         for (int u = 0; u < kUnr; ++u) {
-            const int64_t w = 4 * (kb + u) + j;
+            const int64_t w = D::WPK * (kb + u) + j;
             wv[u] = (real && kb + u < kb1 && w < nw) ? __ldcs(reinterpret_cast<const unsigned long long*>(src + w))
                                                      : 0ull;
         }
@@ -255,12 +179,13 @@ unpack_fp4_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t 
         for (int u = 0; u < kUnr; ++u) {
             if (active && kb + u < kb1) {
                 cnt += __popcll(wv[u]);
-                store_fp4_word(xc + (kb + u) * kb_stride, wv[u]);
+                if constexpr (FP4) store_fp4_word(xc + (kb + u) * kb_stride, wv[u]);
+                else store_int8_word(xc + (kb + u) * kb_stride, wv[u]);
             }
         }
     }
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+#pragma unroll
+    for (int o = 1; o < D::WPK; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (j == 0 && real && cnt) atomicAdd(&colstat[c].vi, (int)cnt);
 }
 
@@ -292,23 +217,22 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
                                 cudaStream_t stream, const int32_t* perm) {
     if (c_begin % kUnpackCols || c_end > m_pad || c_begin >= c_end) return cudaErrorInvalidValue;
     const int fix_s = xlogx_scale(n_rows);
-    const int64_t wpad = ld / 128 * (fp4 ? 4 : 2);
-    const int64_t chunks = (wpad + kUnpackTiles * kUnpackWords - 1) / (kUnpackTiles * kUnpackWords);
-    if (chunks > 65535) return cudaErrorInvalidValue;
-    const dim3 grid((unsigned)((c_end - c_begin + kUnpackCols - 1) / kUnpackCols), (unsigned)chunks);
-    if (fp4) {
-        const int64_t nkb = ld / 128;
+    {
         // tools/unpack_bench.py sweeps (r01h, r01m): 32 k-blocks per block and 16
         // loads in flight per thread were best across configs 3-5 (the kernel
         // is memory-latency bound at 50% occupancy: ncu long-scoreboard stalls)
         constexpr int KB = 32, UNR = 16;
-        const dim3 g2((unsigned)((c_end - c_begin + kDirectCols - 1) / kDirectCols), (unsigned)((nkb + KB - 1) / KB));
+        const int64_t nkb = ld / 128;
+        const int cols = fp4 ? DirectShape<true>::COLS : DirectShape<false>::COLS;
+        const dim3 g2((unsigned)((c_end - c_begin + cols - 1) / cols), (unsigned)((nkb + KB - 1) / KB));
         if (g2.y > 65535) return cudaErrorInvalidValue;
-        unpack_fp4_direct_kernel<KB, UNR><<<g2, 256, 0, stream>>>(words, m, nw, x, nkb, m_pad, colstat, block_mask,
-                                                                   tile, perm, c_begin, c_end);
-    } else
-        unpack_kernel<false><<<grid, 256, 0, stream>>>(words, m, nw, x, ld, m_pad, colstat, block_mask, tile, perm,
-                                                       c_begin);
+        if (fp4)
+            unpack_direct_kernel<true, KB, UNR><<<g2, 256, 0, stream>>>(words, m, nw, x, nkb, m_pad, colstat,
+                                                                        block_mask, tile, perm, c_begin, c_end);
+        else
+            unpack_direct_kernel<false, KB, UNR><<<g2, 256, 0, stream>>>(words, m, nw, x, nkb, m_pad, colstat,
+                                                                         block_mask, tile, perm, c_begin, c_end);
+    }
     int64_t cb = (c_end - c_begin + 255) / 256;
     if (cb > (int64_t)num_sms * 8) cb = (int64_t)num_sms * 8;
     colstat_kernel<<<(unsigned)cb, 256, 0, stream>>>(n_rows, m, c_begin, c_end, colsum, colstat, fix_s, blkrange);
