@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:gram_mi_kernel -s 3 -c 1 \
     -o gpurun_out/${tag}_fused python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
     > gpurun_out/${tag}_ncu_fused.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"unpack_fp4_direct|unpack_kernel" -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"unpack_direct|unpack_fp4_direct|unpack_kernel" -s 3 -c 1 \
     -o gpurun_out/${tag}_unpack python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
     > gpurun_out/${tag}_ncu_unpack.log 2>&1
 echo profile_round done
