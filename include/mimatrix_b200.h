@@ -220,7 +220,7 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * "shard" (8 ranks: 1 = column-group pairs, default; 0 = round robin),
  * "hybrid" (exact-mode tiles off the table path: 0 = FP64, default; 1 = three
  * table gathers + T(c00) computed -- slower on every config measured),
- * "unperm_ctas" (CTAs per SM of mi_unpermute: 1 default, 2 or 4), "ingest"
+ * "unperm_ctas" (CTAs per SM of mi_unpermute: 0 = auto by row width, default; 1..4), "ingest"
  * (mi_all_pairs_host: S = 1..16 column groups uploaded, unpacked, computed and
  * copied back in a pipeline, default 4; 0 = one upload, row-band egress),
  * "ingest_split" (0 = even group sizes, default; 1 = doubling), "serp" (1 =

@@ -70,7 +70,7 @@ Tuning& tuning() {
                        env_int("MI_B200_FIXED", 1), env_int("MI_B200_TABLE_THR", 4096),
                        env_int("MI_B200_PACE", -1), env_int("MI_B200_TAIL", 1), env_int("MI_B200_FP4", 1),
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
-                       env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 1),
+                       env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
                        env_int("MI_B200_SERP", 0)};
     return t;
@@ -803,7 +803,16 @@ int mi_unpermute(const void* d_in, int64_t ld_in, void* d_out, int64_t ld_out, i
     int dev = 0, smem = 0;
     MI_CUDA(cudaGetDevice(&dev));
     MI_CUDA(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const int ctas = tuning().unperm_ctas;
+    // CTAs per SM: the knob, or (0 = auto, default) as many whole source rows
+    // as the SM's shared memory holds, up to 4, for rows up to 90 KB -- more
+    // rows in flight per SM for narrower matrices (tools/unpermute_bench.py:
+    // m = 5000 float64 0.125 -> 0.088 ms, m = 10000 float32 0.215 -> 0.174 ms),
+    // one CTA for wider rows (m = 25000 float32 was slower with two).
+    int ctas = tuning().unperm_ctas;
+    if (ctas == 0) {
+        const int64_t row = n_cols * esz + 1024;
+        ctas = row > 90 * 1024 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(4, (int64_t)smem / row));
+    }
     int per_cta = smem / ctas - 1024;  // leave room for the per-CTA reserve
     per_cta = per_cta / 16 * 16;
     MI_CUDA(launch_unpermute(d_in, ld_in, d_out, ld_out, n_cols, esz, d_inv, info.num_sms, per_cta, ctas,
@@ -1418,7 +1427,7 @@ int mi_set_tuning(const char* key, int value) {
         if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "ingest_split must be 0 (even) or 1 (doubling)");
         t.ingest_split = value;
     } else if (!strcmp(key, "unperm_ctas")) {
-        if (value != 1 && value != 2 && value != 4) return fail(MI_ERR_DOMAIN, "unperm_ctas must be 1, 2 or 4");
+        if (value < 0 || value > 4) return fail(MI_ERR_DOMAIN, "unperm_ctas must be 0 (auto) or 1..4");
         t.unperm_ctas = value;
     } else if (!strcmp(key, "epi_warps")) {
         if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");

@@ -23,6 +23,7 @@
 //                      HBM-bound: m^2 esz read + m^2 esz written.
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -243,7 +244,7 @@ cudaError_t launch_unpermute(const void* in, int64_t ld_in, void* out, int64_t l
     const size_t shm = (size_t)chunk * esz;
     int64_t grid = (int64_t)num_sms * ctas_per_sm;
     if (grid > m) grid = m;
-    const int threads = 512 / ctas_per_sm < 128 ? 128 : 512 / ctas_per_sm;
+    const int threads = std::max(128, 512 / ctas_per_sm / 32 * 32);
     cudaError_t e;
     if (esz == 8) {
         if ((e = cudaFuncSetAttribute(unpermute_kernel<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,

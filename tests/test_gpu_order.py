@@ -85,7 +85,7 @@ def test_unpermute_multi_chunk_rows(engine):
         il = inv.long()
         assert torch.equal(out, src.index_select(0, il).index_select(1, il))
     finally:
-        nat.set_tuning(unperm_ctas=1)
+        nat.set_tuning(unperm_ctas=0)
 
 
 def test_unpermute_rejects_bad_arguments(engine):

@@ -13,7 +13,7 @@ from paper_2411_19702_b200 import _native as nat
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="4")
-ap.add_argument("--unperm-ctas", default="1")
+ap.add_argument("--unperm-ctas", default="0")
 a = ap.parse_args()
 eng = MIEngine.get(0)
 dev = eng.device
@@ -58,7 +58,7 @@ for cfg in [int(x) for x in a.configs.split(",")]:
         r[f"unpermute_ms_ctas{c}"] = timed(lambda: nat.lib().mi_unpermute(slot.data_ptr(), m, out.data_ptr(), m, m,
                                                                           slot.element_size(), prep.inv.data_ptr(), st),
                                            reps)
-    nat.set_tuning(unperm_ctas=1)
+    nat.set_tuning(unperm_ctas=0)
     del slot
     torch.cuda.empty_cache()
     r["colsum_step_ms"] = timed(lambda: eng.compute(eng.prepare(w, n, m, order="colsum"), None, dt, out=out), reps)
