@@ -226,3 +226,25 @@ def test_staged_broadcast_plan():
     assert dispatch.auto_stages(50_000, 8, 148) == 4     # config 4: ~33 rounds per rank
     assert dispatch.auto_stages(10_000, 8, 148) == 1     # config 3: ~1.4 rounds per rank
     assert dispatch.auto_stages(10_000, 2, 148) == 1
+
+
+def test_every_documented_knob_round_trips():
+    """Each knob the header documents is accepted, read back, and range-checked
+    (host logic; no device needed)."""
+    from paper_2411_19702_b200.errors import DomainError
+
+    good = {"cta_group": 1, "prefetch": 4, "l2_hint": 0, "band": 3, "stages": 6, "epi_warps": 8, "fixed": 0,
+            "table_thr": 1000, "pace": 16, "tail": 2, "fp4": 0, "evac": 2, "shard": 0, "hybrid": 1,
+            "unperm_ctas": 2, "ingest": 6, "ingest_split": 1, "serp": 1}
+    bad = {"ingest": 17, "ingest_split": 2, "serp": 2, "unperm_ctas": 5, "evac": 3, "tail": 4}
+    old = {k: nat.get_tuning(k) for k in good}
+    try:
+        for k, v in good.items():
+            nat.set_tuning(**{k: v})
+            assert nat.get_tuning(k) == v, k
+        for k, v in bad.items():
+            with pytest.raises(DomainError):
+                nat.set_tuning(**{k: v})
+    finally:
+        for k, v in old.items():
+            nat.set_tuning(**{k: v})
