@@ -61,7 +61,7 @@ int env_int(const char* name, int dflt) {
 }
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid, unperm_ctas, ingest, ingest_split, serp;
+        hybrid, unperm_ctas, ingest, ingest_split, serp, f32_epi;
 };
 Tuning& tuning() {
     static Tuning t = {env_int("MI_B200_CTA_GROUP", 2) == 1 ? 1 : 2, env_int("MI_B200_PREFETCH", 0),
@@ -72,7 +72,7 @@ Tuning& tuning() {
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
-                       env_int("MI_B200_SERP", 0)};
+                       env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -893,6 +893,8 @@ int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, 
     p.table_thr = tuning().fixed == 0 ? -1 : tuning().fixed == 2 ? 0x7FFFFFFF : tuning().fixed == 3 ? -1 : tuning().table_thr;
     // tiles that miss the table threshold: hybrid (fixed 1 with hybrid on, or 3) or FP64
     p.hybrid = (tuning().fixed == 3 || (tuning().fixed == 1 && tuning().hybrid)) && p.fix_r ? 1 : 0;
+    // float32 output: the FP32-pipe epilogue for those tiles (counts exact in fp32: N < 2^24)
+    p.f32_epi = (tuning().f32_epi && tuning().fixed != 0 && out_kind == MI_OUT_F32 && n_rows < kFp4MaxN) ? 1 : 0;
     int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
     MI_CUDA(launch_gram_mi(cta_group(), operand_fp4(n_rows), out_kind, eff_mode, tuning().stages, tuning().epi_warps,
@@ -1429,6 +1431,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "unperm_ctas")) {
         if (value < 0 || value > 4) return fail(MI_ERR_DOMAIN, "unperm_ctas must be 0 (auto) or 1..4");
         t.unperm_ctas = value;
+    } else if (!strcmp(key, "f32_epi")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "f32_epi must be 0 (FP64) or 1 (FP32 pipe)");
+        t.f32_epi = value;
     } else if (!strcmp(key, "epi_warps")) {
         if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");
         t.epi_warps = value;
@@ -1459,6 +1464,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "ingest")) return t.ingest;
     if (!strcmp(key, "ingest_split")) return t.ingest_split;
     if (!strcmp(key, "serp")) return t.serp;
+    if (!strcmp(key, "f32_epi")) return t.f32_epi;
     return -1;
 }
 

@@ -248,70 +248,13 @@ __device__ __forceinline__ void st1h(int32_t* p, int32_t v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
 }
 
-// The tile row's fixed-point marginals (table path).
-struct RowQ {
-    int v, nmv;      // v_i, N - v_i
-    long long kq;    // T(N) - (T(v_i) + T(N - v_i))
-};
-
-// 16 columns of one output row (this thread's TMEM lane): MI (or counts), the
-// coalesced mirror store of column i and the direct store of row i.
-// TABLE: exact mode through the fixed-point c log2 c table (integer sums, no
-// FP64 -- B200 runs FP64 on the tensor datapath, ~23x slower under tcgen05.mma);
-// otherwise the FP64 epilogue (epsilon mode, and exact-mode tiles whose column
-// sums are too spread out for the table gathers to stay in L1).
-// HYB (with TABLE): the hybrid path -- T(g), T(a - g), T(b - g) gathered, T(c00)
-// evaluated by the table's own generating function fix_xlog2x (bit-identical to
-// the entry, so exactness is unchanged): c00 = N - a - b + g is the one
-// argument that scatters over the table when column sums are spread, and its
-// L1 misses are what rules the full table out for such tiles.
-template <int OUT, int MODE, bool DIAG, bool TABLE, bool HYB, typename T>
-__device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A, const RowQ& AQ,
-                                           const ColS* __restrict__ cols, const ColS& Arow,
-                                           const GramMiParams& p, double eN, double fN, double dN, double rN,
-                                           const double2* __restrict__ tab, T* __restrict__ out, int64_t ld,
-                                           bool row_ok, bool vec_ok) {
+// The epilogue's stores of 16 finished values of row i, columns j0 .. j0+15:
+// the coalesced mirror store of column i and the direct store of row i (or
+// the packed upper triangle).
+template <bool DIAG, typename T>
+__device__ __forceinline__ void store16(const T (&v)[16], int i, int j0, const GramMiParams& p,
+                                        T* __restrict__ out, int64_t ld, bool row_ok, bool vec_ok) {
     const int m = p.m;
-    // 1) all 16 values into registers first: independent chains (and table
-    //    gathers) the scheduler can overlap, no stores in between
-    T v[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const int j = j0 + k;
-        if constexpr (OUT == MI_OUT_COUNTS) {
-            v[k] = (T)r[k];
-        } else if constexpr (TABLE) {
-            // integer sum of fixed-point terms: exact and order-independent, so
-            // both halves of a diagonal tile agree bit for bit
-            const int g = (int)r[k];
-            const int bv = cols[k].vi;
-            const long long* __restrict__ X = p.xlogx;
-            const long long t00 = HYB ? fix_xlog2x((unsigned)(AQ.nmv - bv + g), p.fix_s, p.fix_r, p.fix_lg)
-                                      : __ldg(X + (AQ.nmv - bv + g));
-            const long long S = (__ldg(X + g) + __ldg(X + (AQ.v - g))) + (__ldg(X + (bv - g)) + t00) +
-                                (AQ.kq - cols[k].q);
-            T x = fixed_to_fp<T>(S, p.rcp, p.off0);
-            if (DIAG && !p.include_diagonal && i == j) x = (T)0;
-            v[k] = x;
-        } else {
-            const double g = u32_to_double(r[k]);
-            const ColS& B = cols[k];
-            double x;
-            if constexpr (MODE == MI_MODE_EXACT) {
-                if (DIAG && j < i) {
-                    // (min, max) orientation: the two halves of a diagonal
-                    // tile are then bit-identical mirrors
-                    x = mi_exact<OUT == MI_OUT_F32>(g, row_marg(B, eN, dN), Arow, fN, dN, rN, tab);
-                } else {
-                    x = mi_exact<OUT == MI_OUT_F32>(g, A, B, fN, dN, rN, tab);
-                }
-            } else {
-                x = (DIAG && j < i) ? mi_epsilon(g, B.v, A.v, dN, p.eps) : mi_epsilon(g, A.v, B.v, dN, p.eps);
-            }
-            if (DIAG && !p.include_diagonal && i == j) x = 0.0;
-            v[k] = (T)x;
-        }
-    }
     if (p.debug & 1) {  // keep the math alive without storing the tile
         T acc = v[0];
 #pragma unroll
@@ -365,6 +308,94 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
             if (j0 + k + 1 < m) dst[k + 1] = v[k + 1];
         }
     }
+}
+
+// The tile row's fixed-point marginals (table path).
+struct RowQ {
+    int v, nmv;      // v_i, N - v_i
+    long long kq;    // T(N) - (T(v_i) + T(N - v_i))
+};
+
+// 16 columns of one output row (this thread's TMEM lane): MI (or counts), the
+// coalesced mirror store of column i and the direct store of row i.
+// TABLE: exact mode through the fixed-point c log2 c table (integer sums, no
+// FP64 -- B200 runs FP64 on the tensor datapath, ~23x slower under tcgen05.mma);
+// otherwise the FP64 epilogue (epsilon mode, and exact-mode tiles whose column
+// sums are too spread out for the table gathers to stay in L1).
+// HYB (with TABLE): the hybrid path -- T(g), T(a - g), T(b - g) gathered, T(c00)
+// evaluated by the table's own generating function fix_xlog2x (bit-identical to
+// the entry, so exactness is unchanged): c00 = N - a - b + g is the one
+// argument that scatters over the table when column sums are spread, and its
+// L1 misses are what rules the full table out for such tiles.
+template <int OUT, int MODE, bool DIAG, bool TABLE, bool HYB, typename T>
+__device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j0, const RowMarg& A, const RowQ& AQ,
+                                           const ColS* __restrict__ cols, const ColS& Arow,
+                                           const GramMiParams& p, double eN, double fN, double dN, double rN,
+                                           const double2* __restrict__ tab, T* __restrict__ out, int64_t ld,
+                                           bool row_ok, bool vec_ok) {
+    // 1) all 16 values into registers first: independent chains (and table
+    //    gathers) the scheduler can overlap, no stores in between
+    T v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int j = j0 + k;
+        if constexpr (OUT == MI_OUT_COUNTS) {
+            v[k] = (T)r[k];
+        } else if constexpr (TABLE) {
+            // integer sum of fixed-point terms: exact and order-independent, so
+            // both halves of a diagonal tile agree bit for bit
+            const int g = (int)r[k];
+            const int bv = cols[k].vi;
+            const long long* __restrict__ X = p.xlogx;
+            const long long t00 = HYB ? fix_xlog2x((unsigned)(AQ.nmv - bv + g), p.fix_s, p.fix_r, p.fix_lg)
+                                      : __ldg(X + (AQ.nmv - bv + g));
+            const long long S = (__ldg(X + g) + __ldg(X + (AQ.v - g))) + (__ldg(X + (bv - g)) + t00) +
+                                (AQ.kq - cols[k].q);
+            T x = fixed_to_fp<T>(S, p.rcp, p.off0);
+            if (DIAG && !p.include_diagonal && i == j) x = (T)0;
+            v[k] = x;
+        } else {
+            const double g = u32_to_double(r[k]);
+            const ColS& B = cols[k];
+            double x;
+            if constexpr (MODE == MI_MODE_EXACT) {
+                if (DIAG && j < i) {
+                    // (min, max) orientation: the two halves of a diagonal
+                    // tile are then bit-identical mirrors
+                    x = mi_exact<OUT == MI_OUT_F32>(g, row_marg(B, eN, dN), Arow, fN, dN, rN, tab);
+                } else {
+                    x = mi_exact<OUT == MI_OUT_F32>(g, A, B, fN, dN, rN, tab);
+                }
+            } else {
+                x = (DIAG && j < i) ? mi_epsilon(g, B.v, A.v, dN, p.eps) : mi_epsilon(g, A.v, B.v, dN, p.eps);
+            }
+            if (DIAG && !p.include_diagonal && i == j) x = 0.0;
+            v[k] = (T)x;
+        }
+    }
+    store16<DIAG>(v, i, j0, p, out, ld, row_ok, vec_ok);
+}
+
+// 16 columns of one output row through the float32 epilogue (f32_mi,
+// milog.cuh): FP32 pipe only, so it overlaps the next tile's MMAs.  Diagonal
+// tiles evaluate (min, max) orientations so the two halves are bit-identical.
+// RAW: r holds the fp32 accumulator words themselves (exact integer counts),
+// else integer counts (K-split partial sums, int8 accumulators).
+template <bool DIAG, bool RAW>
+__device__ __forceinline__ void epilogue16_f32(const uint32_t (&r)[16], int i, int j0, const ColF& Af,
+                                               const ColF* __restrict__ cols, const GramMiParams& p, float dN,
+                                               float rN, float* __restrict__ out, int64_t ld, bool row_ok,
+                                               bool vec_ok) {
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const float g = RAW ? __uint_as_float(r[k]) : __uint2float_rn(r[k]);  // exact: counts < 2^24
+        const int j = j0 + k;
+        float x = (DIAG && j < i) ? f32_mi(g, cols[k], Af, dN, rN) : f32_mi(g, Af, cols[k], dN, rN);
+        if (DIAG && !p.include_diagonal && i == j) x = 0.0f;
+        v[k] = x;
+    }
+    store16<DIAG>(v, i, j0, p, out, ld, row_ok, vec_ok);
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -556,14 +587,19 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 
     if (warp == 0) {
         // ================= TMA producer =================
+        // The whole warp runs the loop (warp-uniform control flow: descriptors
+        // and coordinates stay in uniform registers) and one elected lane
+        // issues.  Under a concurrent epilogue the producer and MMA warps get
+        // a fraction of their schedulers' issue slots, so the per-k-block
+        // instruction path is kept short.
+        const uint64_t policy = p.l2_hint == 1   ? l2_policy_evict_last()
+                                : p.l2_hint == 2 ? l2_policy_evict_first()
+                                                 : l2_policy_evict_normal();
+        const int pf = p.prefetch_dist;
+        const uint32_t fb_rank = (CG == 2) ? 0u : rank;  // CG == 2: signal the leader's barrier
+        int s = 0;
+        uint32_t ph = 0;
         if (lane == 0) {
-            const uint64_t policy = p.l2_hint == 1   ? l2_policy_evict_last()
-                                    : p.l2_hint == 2 ? l2_policy_evict_first()
-                                                     : l2_policy_evict_normal();
-            const int pf = p.prefetch_dist;
-            const uint32_t fb_rank = (CG == 2) ? 0u : rank;  // CG == 2: signal the leader's barrier
-            int s = 0;
-            uint32_t ph = 0;
             for (long long g = 0; g < pf; ++g) {  // warm the L2 with the first pf k-blocks
                 int t, kb;
                 if (!walk.at(g, t, kb)) break;
@@ -571,12 +607,28 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 tma_prefetch_3d(&tmap_x, 0, tile.x * C::TS + (int)rank * 128, kb);
                 tma_prefetch_3d(&tmap_x, 0, tile.y * C::TS + (int)rank * 128, kb);
             }
-            int t, kb;
-            bool pace_on = pacing;
-            const long long win = p.pace_window;
-            for (long long g = 0; walk.at(g, t, kb); ++g) {
+        }
+        bool pace_on = pacing;
+        const long long win = p.pace_window;
+        // tile loop outside, k-block loop inside: the tile's coordinates are
+        // loaded once per tile and nothing on the per-k-block path divides or
+        // touches global memory (the epilogue's stores share the LSU with
+        // such loads and would stretch their latency into the MMA's supply)
+        long long g = 0;
+        for (int it = 0;; ++it) {
+            const int t = cluster + it * n_clusters;
+            if (t >= p.n_full) break;
+            const int2 tile = p.tiles[t];
+            const int rowA = tile.x * C::TS + (int)rank * 128;
+            const int rowB = tile.y * C::TS + (int)rank * 128;
+            const bool rev = (walk.serp & it) != 0;
+            const bool ptrc = p.trace && cluster == 0 && it < 64;
+            long long pwait = 0;
+            const long long pt0 = ptrc ? clock64() : 0;
+            for (int k = 0; k < nkb; ++k, ++g) {
+                const int kb = rev ? nkb - 1 - k : k;
                 if (PACE && pace_on && (g & 15) == 0) {
-                    s_pace[0] = (uint32_t)g;
+                    if (lane == 0) s_pace[0] = (uint32_t)g;
                     if (g > win) {
                         // wait (bounded: pacing is only a hint) while the slowest pair is too far behind
                         int spins = 0;
@@ -585,40 +637,59 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                             if (++spins > 20000) { pace_on = false; break; }
                         }
                     }
+                    pace_on = __all_sync(0xFFFFFFFFu, pace_on);
                 }
-                const int2 tile = p.tiles[t];
-                const int rowA = tile.x * C::TS + (int)rank * 128;
-                const int rowB = tile.y * C::TS + (int)rank * 128;
-                int tp, kbp;
-                if (pf > 0 && walk.at(g + pf, tp, kbp)) {
-                    const int2 tpf = p.tiles[tp];
-                    tma_prefetch_3d(&tmap_x, 0, tpf.x * C::TS + (int)rank * 128, kbp);
-                    tma_prefetch_3d(&tmap_x, 0, tpf.y * C::TS + (int)rank * 128, kbp);
+                if (pf > 0 && lane == 0) {
+                    int tp, kbp;
+                    if (walk.at(g + pf, tp, kbp)) {
+                        const int2 tpf = p.tiles[tp];
+                        tma_prefetch_3d(&tmap_x, 0, tpf.x * C::TS + (int)rank * 128, kbp);
+                        tma_prefetch_3d(&tmap_x, 0, tpf.y * C::TS + (int)rank * 128, kbp);
+                    }
                 }
-                mbar_wait(empty_bar(s), ph ^ 1u);
-                const uint32_t fb = (CG == 2) ? map_to_cta(full_bar(s), fb_rank) : full_bar(s);
-                if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
-                tma_load_3d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, 0, rowA, kb, policy);
-                tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
+                if (ptrc) {
+                    const long long w0 = clock64();
+                    mbar_wait(empty_bar(s), ph ^ 1u);
+                    pwait += clock64() - w0;
+                } else {
+                    mbar_wait(empty_bar(s), ph ^ 1u);
+                }
+                if (elect_one()) {
+                    const uint32_t fb = (CG == 2) ? map_to_cta(full_bar(s), fb_rank) : full_bar(s);
+                    if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
+                    tma_load_3d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, 0, rowA, kb, policy);
+                    tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
+                }
+                __syncwarp();
                 if (++s == ST) { s = 0; ph ^= 1u; }
             }
-            if (has_tail) {
-                const uint2 st = producer_tail<CG, ST>(&tmap_x, p.tiles[tail_t], rank, tail_k ? 0 : tail_c, tail_w,
-                                                       tail_kb0, tail_kb1, sA, sB, bar0, policy, s, ph);
-                s = (int)st.x;
-                ph = st.y;
+            if (ptrc && lane == 0) {
+                p.trace[1280 + it * 4 + 1 + (int)rank] = pwait;  // producer waiting for free stages
+                p.trace[1280 + it * 4 + 3] = clock64() - pt0;
             }
-            s_pace[2] = 1u;
-            // drain: the last commit of every stage must land before exit
-            for (int q = 0; q < ST; ++q) {
-                mbar_wait(empty_bar(s), ph ^ 1u);
-                if (++s == ST) { s = 0; ph ^= 1u; }
-            }
+        }
+        if (has_tail) {
+            uint2 st = make_uint2((uint32_t)s, ph);
+            if (lane == 0)
+                st = producer_tail<CG, ST>(&tmap_x, p.tiles[tail_t], rank, tail_k ? 0 : tail_c, tail_w, tail_kb0,
+                                           tail_kb1, sA, sB, bar0, policy, s, ph);
+            s = (int)__shfl_sync(0xFFFFFFFFu, st.x, 0);
+            ph = __shfl_sync(0xFFFFFFFFu, st.y, 0);
+        }
+        if (lane == 0) s_pace[2] = 1u;
+        // drain: the last commit of every stage must land before exit
+        for (int q = 0; q < ST; ++q) {
+            mbar_wait(empty_bar(s), ph ^ 1u);
+            if (++s == ST) { s = 0; ph ^= 1u; }
         }
     } else if (warp == 1) {
         // ================= MMA issuer =================
-        if (rank == 0 && lane == 0) {
+        // (warp-uniform loop, one elected lane issues; see the producer)
+        if (rank == 0) {
             constexpr uint32_t idesc = mma_idesc<CG, FP4>(C::MMA_M, C::MMA_N);
+            // stage s's descriptors: base + s * 16 KB (address field in 16-byte units)
+            const uint64_t adesc0 = umma_desc_sw128_kmajor(sA);
+            const uint64_t bdesc0 = umma_desc_sw128_kmajor(sB);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
@@ -627,29 +698,46 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             for (int t = cluster; t < p.n_full; t += n_clusters, ++it) {
                 mbar_wait(tempty_bar(acc), aph ^ 1u);
                 tc_fence_after();
-                if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 0] = clock64();
+                const bool trc = p.trace && cluster == 0 && it < 64;
+                if (trc && lane == 0) p.trace[it * 4 + 0] = clock64();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+                long long wait_cyc = 0;
                 for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(full_bar(s), ph);
-                    tc_fence_after();
-                    const uint64_t adesc = umma_desc_sw128_kmajor(sA + s * kStageHalfBytes);
-                    const uint64_t bdesc = umma_desc_sw128_kmajor(sB + s * kStageHalfBytes);
-                    if (!(p.debug & 16)) {  // debug 16: data movement only (no MMAs)
-#pragma unroll
-                        for (int k = 0; k < kBK / 32; ++k) {
-                            // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
-                            mma_step<CG, FP4>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, tmem_base,
-                                              (kb | k) != 0 ? 1u : 0u);
-                        }
+                    if (trc) {
+                        const long long w0 = clock64();
+                        mbar_wait(full_bar(s), ph);
+                        wait_cyc += clock64() - w0;
+                    } else {
+                        mbar_wait(full_bar(s), ph);
                     }
-                    umma_commit<CG>(empty_bar(s));  // frees the smem slot (both CTAs)
+                    tc_fence_after();
+                    const uint64_t soff = (uint64_t)(s * (kStageHalfBytes >> 4));
+                    const uint64_t adesc = adesc0 + soff;
+                    const uint64_t bdesc = bdesc0 + soff;
+                    if (elect_one()) {
+                        if (!(p.debug & 16)) {  // debug 16: data movement only (no MMAs)
+#pragma unroll
+                            for (int k = 0; k < kBK / 32; ++k) {
+                                // advance 32 bytes (one K=32 int8 step) inside the swizzle atom
+                                mma_step<CG, FP4>(d_tmem, adesc + 2u * k, bdesc + 2u * k, idesc, tmem_base,
+                                                  (kb | k) != 0 ? 1u : 0u);
+                            }
+                        }
+                        umma_commit<CG>(empty_bar(s));  // frees the smem slot (both CTAs)
+                    }
+                    __syncwarp();
                     if (++s == ST) { s = 0; ph ^= 1u; }
                 }
-                umma_commit<CG>(tfull_bar(acc));  // accumulator ready (both CTAs)
-                if (p.trace && cluster == 0 && it < 64) p.trace[it * 4 + 1] = clock64();
+                if (elect_one()) umma_commit<CG>(tfull_bar(acc));  // accumulator ready (both CTAs)
+                __syncwarp();
+                if (trc && lane == 0) {
+                    p.trace[it * 4 + 1] = clock64();
+                    p.trace[1280 + it * 4 + 0] = wait_cyc;  // MMA starved of operands
+                }
                 if (++acc == NACC) { acc = 0; aph ^= 1u; }
             }
-            if (has_tail) mma_tail<CG, ST, FP4>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
+            if (has_tail && lane == 0)
+                mma_tail<CG, ST, FP4>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
         }
     } else if (PACE && warp == C::PACER_WARP) {
         // ================= pacer =================
@@ -681,6 +769,8 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         const int m = p.m;
         const double dN = (double)p.n_rows;
         const double rN = 1.0 / dN;
+        const float dNf = (float)p.n_rows;           // float32 path (N < 2^24: exact)
+        const float rNf = (float)rN;
         named_barrier_sync(1, EW * 32);                  // log2 table is in smem
         int eNi;
         const double fN = log2_frac(dN, tab, eNi);       // same routine as the per-column logs
@@ -713,15 +803,14 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             cpar ^= 1;
             ColS Arow{};
             RowQ AQ{0, 0, 0};
-            bool use_table = false, use_hybrid = false;
+            ColF Af{};
+            ColF* const colsf = reinterpret_cast<ColF*>(cols);  // the float32 path's staging (same buffer)
+            bool use_table = false, use_hybrid = false, use_f32 = false;
             if constexpr (OUT != MI_OUT_COUNTS) {
-                if (etid < C::TS) cols[etid] = col_s(p.colstat[tile.y * C::TS + etid]);
-                named_barrier_sync(2, EW * 32);
-                Arow = col_s(p.colstat[i]);  // colstat has m_pad entries
-                AQ = RowQ{Arow.vi, p.n_rows - Arow.vi, nln - Arow.q};
                 // per-tile choice (identical in both CTAs of a pair): table path
                 // when the tile's column sums are clustered enough for the
-                // gathers to hit in L1, FP64 path otherwise
+                // gathers to hit in L1; otherwise the float32 epilogue for
+                // float32 output, else FP64
                 if (have_table) {
                     const int bl = C::TS / 128;
                     int lo = 0x7FFFFFFF, hi = -1, spread = 0;
@@ -740,7 +829,18 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     }
                     spread += hi >= lo ? hi - lo : 0;
                     use_table = spread <= p.table_thr;
-                    use_hybrid = !use_table && p.hybrid;
+                }
+                use_f32 = OUT == MI_OUT_F32 && MODE == MI_MODE_EXACT && p.f32_epi && !use_table;
+                use_hybrid = have_table && !use_table && !use_f32 && p.hybrid;
+                if (use_f32) {
+                    if (etid < C::TS) colsf[etid] = p.colstat[tile.y * C::TS + etid].f;
+                    named_barrier_sync(2, EW * 32);
+                    Af = p.colstat[i].f;
+                } else {
+                    if (etid < C::TS) cols[etid] = col_s(p.colstat[tile.y * C::TS + etid]);
+                    named_barrier_sync(2, EW * 32);
+                    Arow = col_s(p.colstat[i]);  // colstat has m_pad entries
+                    AQ = RowQ{Arow.vi, p.n_rows - Arow.vi, nln - Arow.q};
                 }
             }
             const RowMarg A = row_marg(Arow, eN, dN);
@@ -753,7 +853,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             // running MMAs is throttled ~23x (r01_micro.md), so FP64-path tiles keep
             // the accumulator until done and run their epilogue alone.
             const bool EVAC = FP4 && TAIL == 0 && p.evac != 0 &&
-                              (OUT == MI_OUT_COUNTS || use_table || use_hybrid || p.evac == 2);
+                              (OUT == MI_OUT_COUNTS || use_table || use_hybrid || use_f32 || p.evac == 2);
             uint32_t keep[16];  // EVAC: the accumulator columns that do not fit the spare TMEM
             if (EVAC) {
 #pragma unroll 1
@@ -792,7 +892,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     tmem_ld_32x32b_x16(tmem_base + lane_q + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
                     tmem_ld_wait(r);
                 }
-                acc_to_counts<FP4>(r);
+                if (!(FP4 && use_f32 && TAIL != 2)) acc_to_counts<FP4>(r);  // (the f32 path reads fp32 counts as is)
                 if constexpr (TAIL == 2) {  // + the other K ranges (integer adds: exact in any order)
                     const int u0 = (t - p.n_full) * p.tail_split;
                     const size_t off = ((size_t)((tc0 + col0) / 16) * 128 + row_local) * 16;
@@ -814,7 +914,17 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     }
                 }
                 const bool vec_ok = ((reinterpret_cast<uintptr_t>(out + (int64_t)i * ld + j0) & (2 * sizeof(T) - 1)) == 0);
-                if (use_table) {
+                if (use_f32) {
+                    if constexpr (MODE == MI_MODE_EXACT && OUT == MI_OUT_F32) {
+                        constexpr bool RAW = FP4 && TAIL != 2;
+                        if (diag)
+                            epilogue16_f32<true, RAW>(r, i, j0, Af, colsf + c0 + col0, p, dNf, rNf, out, ld, row_ok,
+                                                      vec_ok);
+                        else
+                            epilogue16_f32<false, RAW>(r, i, j0, Af, colsf + c0 + col0, p, dNf, rNf, out, ld, row_ok,
+                                                       vec_ok);
+                    }
+                } else if (use_table) {
                     if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
                         if (diag)
                             epilogue16<OUT, MODE, true, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,

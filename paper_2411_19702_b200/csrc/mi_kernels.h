@@ -39,6 +39,8 @@ struct GramMiParams {
     const int2* blkrange;   // exact mode: (min, max) column sum per 128-column block
     int table_thr;          // table path when the tile's two column-sum ranges sum to <= this
     int hybrid;             // other exact-mode tiles: 1 = hybrid (3 table gathers + T(c00) computed), 0 = FP64
+    int f32_epi;            // float32 output, exact mode: tiles off the table path run the FP32-pipe
+                            // epilogue (f32_mi, milog.cuh) instead of FP64, evacuated like the table path
     const float* fix_r;     // fix_xlog2x mantissa tables in global memory (hybrid path)
     const float2* fix_lg;
     unsigned int* row_done; // optional: per tile row I, +1 per CTA when its part of tile (I, J) is

@@ -75,6 +75,18 @@ __device__ __forceinline__ void write_colstat(int64_t c, uint32_t cnt, int64_t n
     st.vi = (int)cnt;
     st.pad = 0;
     st.q = fix_xlog2x(cnt, fix_s, kFixR, kFixLG) + fix_xlog2x((unsigned)v0, fix_s, kFixR, kFixLG);
+    // float32 epilogue factors: N / a and 1 / a as float pairs (1.0 for a = 0)
+    const double dn = (double)n_rows;
+    auto split = [](double x, float& hi, float& lo) {
+        hi = (float)x;
+        lo = (float)(x - (double)hi);
+    };
+    st.f.v = (float)cnt;
+    split(cnt > 0 ? dn / (double)cnt : 1.0, st.f.s1h, st.f.s1l);
+    split(v0 > 0 ? dn / (double)v0 : 1.0, st.f.s0h, st.f.s0l);
+    split(cnt > 0 ? 1.0 / (double)cnt : 1.0, st.f.t1h, st.f.t1l);
+    split(v0 > 0 ? 1.0 / (double)v0 : 1.0, st.f.t0h, st.f.t0l);
+    st.f.pad[0] = st.f.pad[1] = st.f.pad[2] = 0.f;
     colstat[c] = st;
     if (blkrange) {
         // per-128-column (min, max) of the real columns: one atomic pair per

@@ -55,8 +55,8 @@ def test_layout_helpers():
     assert lib.mi_tile_size() in (128, 256)
     T = -(-10000 // lib.mi_tile_size())
     assert lib.mi_num_tiles(10000) == T * (T + 1) // 2
-    assert lib.mi_colstat_bytes(1000, 300) == 512 * 64 + 1001 * 8 + 4 * 8 + 1024 * 12
-    assert lib.mi_colstat_bytes(1 << 25, 300) == 512 * 64
+    assert lib.mi_colstat_bytes(1000, 300) == 512 * 112 + 1001 * 8 + 4 * 8 + 1024 * 12
+    assert lib.mi_colstat_bytes(1 << 25, 300) == 512 * 112
 
 
 @pytest.mark.parametrize("m", [1, 255, 256, 257, 1000, 10000, 50000])
