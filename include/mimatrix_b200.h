@@ -224,12 +224,24 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * (mi_all_pairs_host: S = 1..16 column groups uploaded, unpacked, computed and
  * copied back in a pipeline, default 4; 0 = one upload, row-band egress),
  * "ingest_split" (0 = even group sizes, default; 1 = doubling), "serp" (1 =
- * odd tile rounds sweep K backwards for L2 reuse across rounds; 0 default).  Also
+ * odd tile rounds sweep K backwards for L2 reuse across rounds; 0 default),
+ * "f32_epi" (float32 output, exact mode: tiles off the table path run the
+ * FP32-pipe epilogue beside the next tile's MMAs; 1 default, 0 = FP64).  Also
  * settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */
 /* release the cached device workspaces of mi_*_host */
 void mi_release_workspace(void);
+
+/* Measured tensor peak of this device (the roofline denominator of the fused
+ * kernel): every SM pair issues tcgen05.mma.cta_group::2 M=256 N=256 back to
+ * back on shared-memory-resident operands -- kind::mxf4 with unit scales
+ * (fp4 = 1, the fused kernel's instruction below 2^24 rows) or kind::i8
+ * (fp4 = 0) -- for about `seconds` (short = burst clocks, >= 1 s = sustained
+ * under the power cap).  Outputs (any may be NULL): dense tensor ops/s (2 per
+ * MAC), MACs per clock per SM, and the effective SM clock in MHz. */
+int mi_tensor_peak(int device, int fp4, double seconds, double* ops_per_s, double* macs_per_clk_sm,
+                   double* sm_mhz);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,7 @@ SIGNATURES = {
     "mi_set_tuning": (_int, [ctypes.c_char_p, _int]),
     "mi_get_tuning": (_int, [ctypes.c_char_p]),
     "mi_release_workspace": (None, []),
+    "mi_tensor_peak": (_int, [_int, _int, _dbl, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -143,6 +144,17 @@ def set_tuning(**kw) -> None:
 
 def get_tuning(key: str) -> int:
     return int(lib().mi_get_tuning(key.encode()))
+
+
+def tensor_peak(device: int = 0, fp4: bool = True, seconds: float = 0.05) -> dict:
+    """Measured tensor peak of the device (mi_tensor_peak): dense ops/s of the
+    fused kernel's MMA instruction on resident operands, MACs/clk/SM, clock."""
+    ops, macs, mhz = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+    check(lib().mi_tensor_peak(device, 1 if fp4 else 0, seconds, ctypes.byref(ops), ctypes.byref(macs),
+                               ctypes.byref(mhz)), "mi_tensor_peak")
+    return {"ops_per_s": ops.value, "macs_per_clk_sm": macs.value, "sm_mhz": mhz.value, "seconds": seconds,
+            "instruction": "tcgen05.mma.cta_group::2.kind::" + ("mxf4.block_scale.block32" if fp4 else "i8") +
+                           " M256 N256, smem-resident operands, all SM pairs"}
 
 
 def rank_blocks(n_cols: int, rank: int = 0, world: int = 1):

@@ -1,0 +1,624 @@
+// Host-buffer entry points (mi_all_pairs_host and friends): the cached
+// per-device workspace, pinned staging of pageable words with host copy
+// threads, the staged upload -> unpack -> compute -> download pipeline, the
+// row-band egress that overlaps the fused kernel, and the sharded egress.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <algorithm>
+#include <chrono>
+#include <mutex>
+#include <thread>
+#include <condition_variable>
+#include <vector>
+
+#include "../../include/mimatrix_b200.h"
+#include "capi_internal.h"
+#include "mi_kernels.h"
+#include "milog.cuh"
+
+using namespace mib200;
+using namespace mib200::capi;
+
+namespace mib200 {
+namespace capi {
+
+// Grow-only device workspace for the host-buffer entry points.
+struct Workspace {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    void* words = nullptr; size_t words_cap = 0;
+    void* x = nullptr; size_t x_cap = 0;
+    void* colsum = nullptr; size_t colsum_cap = 0;
+    void* colstat = nullptr; size_t colstat_cap = 0;
+    void* tiles = nullptr; size_t tiles_cap = 0;
+    void* out = nullptr; size_t out_cap = 0;
+    void* h_stage = nullptr; size_t h_stage_cap = 0;  // pinned staging of pageable host words
+    cudaStream_t copy_stream = nullptr;   // D2H of finished row bands
+    cudaEvent_t copy_ev[2] = {nullptr, nullptr};  // the last two D2H copies
+    cudaEvent_t stage_ev[kMaxIngestStages] = {};  // staged path: stage g's tiles are stored
+    unsigned int* row_done_h = nullptr;   // pinned, mapped: per tile row completion counts
+    unsigned int* row_done_d = nullptr;   // device alias of row_done_h
+    size_t row_done_cap = 0;
+};
+std::mutex g_ws_mu;
+Workspace g_ws[64];
+
+int ensure(void** p, size_t* cap, size_t need) {
+    if (*cap >= need && *p) return MI_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    MI_CUDA(cudaMalloc(p, need ? need : 16));
+    *cap = need;
+    return MI_OK;
+}
+
+void release(Workspace& w) {
+    if (w.device < 0) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(w.device);
+    void** ps[] = {&w.words, &w.x, &w.colsum, &w.colstat, &w.tiles, &w.out};
+    for (void** p : ps)
+        if (*p) cudaFree(*p), *p = nullptr;
+    w.words_cap = w.x_cap = w.colsum_cap = w.colstat_cap = w.tiles_cap = w.out_cap = 0;
+    if (w.stream) cudaStreamDestroy(w.stream), w.stream = nullptr;
+    if (w.copy_stream) cudaStreamDestroy(w.copy_stream), w.copy_stream = nullptr;
+    for (auto& e : w.copy_ev)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    for (auto& e : w.stage_ev)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    if (w.row_done_h) cudaFreeHost(w.row_done_h), w.row_done_h = nullptr, w.row_done_d = nullptr;
+    if (w.h_stage) cudaFreeHost(w.h_stage), w.h_stage = nullptr;
+    w.h_stage_cap = 0;
+    w.row_done_cap = 0;
+    w.device = -1;
+    cudaSetDevice(prev);
+}
+
+// words (host) -> X, colsum on the device; shared by the host entry points.
+// True when h points into page-locked (or registered / managed) host memory
+// that the copy engines can read directly.
+bool host_is_pinned(const void* h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// memcpy with up to `threads` host threads (pageable -> pinned staging): one
+// thread reaches ~10 GB/s, well short of the link's ~55.  The workers are a
+// small persistent pool (created on first use, never torn down: spawning 8
+// threads per group cost ~1 ms a call); calls are serialised by g_ws_mu.
+struct CopyPool {
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::vector<std::thread> workers;
+    struct Job { char* dst; const char* src; size_t n; };
+    std::vector<Job> jobs;
+    size_t next = 0, pending = 0;
+    void ensure(int n) {
+        while ((int)workers.size() < n) {
+            workers.emplace_back([this] {
+                for (;;) {
+                    Job j;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [this] { return next < jobs.size(); });
+                        j = jobs[next++];
+                    }
+                    memcpy(j.dst, j.src, j.n);
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (--pending == 0) done_cv.notify_all();
+                }
+            });
+            workers.back().detach();
+        }
+    }
+};
+CopyPool& copy_pool() {
+    static CopyPool* p = new CopyPool();  // leaked on purpose: detached workers outlive static destruction
+    return *p;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    const size_t min_chunk = (size_t)4 << 20;
+    const int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
+    if (t <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    CopyPool& pool = copy_pool();
+    pool.ensure(t);
+    const size_t chunk = (bytes + t - 1) / t;
+    {
+        std::lock_guard<std::mutex> lk(pool.mu);
+        pool.jobs.clear();
+        pool.next = 0;
+        for (int i = 0; i < t; ++i) {
+            const size_t o = (size_t)i * chunk;
+            if (o >= bytes) break;
+            pool.jobs.push_back({(char*)dst + o, (const char*)src + o, std::min(chunk, bytes - o)});
+        }
+        pool.pending = pool.jobs.size();
+    }
+    pool.cv.notify_all();
+    std::unique_lock<std::mutex> lk(pool.mu);
+    pool.done_cv.wait(lk, [&] { return pool.pending == 0; });
+}
+
+// H2D of host words into ws.words on ws.stream.  Pageable words (numpy
+// arrays) go through the cached pinned staging buffer in 4 column chunks:
+// host threads copy chunk k while the copy engine moves chunk k - 1 (the
+// driver's own pageable path runs at ~10 GB/s).
+int upload_words(Workspace& ws, const uint64_t* h_words, int64_t n_cols, int64_t nw) {
+    const size_t bytes = (size_t)(n_cols * nw * 8);
+    if (host_is_pinned(h_words)) {
+        MI_CUDA(cudaMemcpyAsync(ws.words, h_words, bytes, cudaMemcpyHostToDevice, ws.stream));
+        return MI_OK;
+    }
+    if (ws.h_stage_cap < bytes) {
+        if (ws.h_stage) cudaFreeHost(ws.h_stage);
+        ws.h_stage = nullptr;
+        ws.h_stage_cap = 0;
+        MI_CUDA(cudaHostAlloc(&ws.h_stage, bytes, cudaHostAllocDefault));
+        ws.h_stage_cap = bytes;
+    }
+    const int threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    const int64_t chunks = n_cols >= 4 ? 4 : 1;
+    for (int64_t k = 0; k < chunks; ++k) {
+        const int64_t c0 = n_cols * k / chunks, c1 = n_cols * (k + 1) / chunks;
+        const size_t off = (size_t)(c0 * nw * 8), len = (size_t)((c1 - c0) * nw * 8);
+        parallel_memcpy((char*)ws.h_stage + off, (const char*)h_words + off, len, threads);
+        MI_CUDA(cudaMemcpyAsync((char*)ws.words + off, (char*)ws.h_stage + off, len, cudaMemcpyHostToDevice,
+                                ws.stream));
+    }
+    return MI_OK;
+}
+
+int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int64_t* ld_out,
+                 int64_t* m_pad_out, const DevInfo& info) {
+    const int64_t nw = (n_rows + 63) / 64;
+    const int64_t ld = mi_kmajor_ld(n_rows);
+    const int64_t m_pad = mi_kmajor_rows(n_cols);
+    int rc;
+    if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
+    if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
+    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
+    if ((rc = upload_words(ws, h_words, n_cols, nw))) return rc;
+    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
+                                 (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
+                                 blkrange_ptr(ws.colstat, n_rows, n_cols), fixr_ptr(ws.colstat, n_rows, n_cols),
+                                 operand_fp4(n_rows), nullptr,
+                                 mi_tile_size(), info.num_sms, ws.stream));
+    *ld_out = ld;
+    *m_pad_out = m_pad;
+    return MI_OK;
+}
+
+int workspace_for(int device, Workspace** out, DevInfo* info) {
+    int rc = query_device(device, info);
+    if (rc) return rc;
+    MI_CUDA(cudaSetDevice(device));
+    Workspace& ws = g_ws[device];
+    if (ws.device < 0) {
+        ws.device = device;
+        MI_CUDA(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+        MI_CUDA(cudaStreamCreateWithFlags(&ws.copy_stream, cudaStreamNonBlocking));
+    }
+    *out = &ws;
+    return MI_OK;
+}
+
+int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t m_pad, int mode, double eps,
+              int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const DevInfo& info,
+              unsigned int* row_done = nullptr) {
+    (void)m_pad;
+    const int64_t n_tiles = mi_num_tiles(n_cols);
+    std::vector<int32_t> tiles = all_tiles(tiles_per_side(n_cols), tile_band(), row_done ? 1 : 0);
+    int rc;
+    if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
+    MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
+    (void)info;
+    return launch_fused((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps, include_diagonal, out_kind,
+                        d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, row_done, ws.stream);
+}
+
+}  // namespace capi
+}  // namespace mib200
+
+extern "C" {
+
+int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                        int include_diagonal, int out_kind, void* h_out, int device, bool packed);
+
+int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                      int include_diagonal, int out_kind, void* h_out, int device) {
+    return all_pairs_host_impl(h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out, device,
+                               false);
+}
+
+int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                             int include_diagonal, int out_kind, void* h_out, int device) {
+    return all_pairs_host_impl(h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out, device,
+                               true);
+}
+
+// Staged ingest -> compute -> egress (full-matrix output): the column blocks
+// are cut into S groups; group g's words go H2D and are unpacked, then the
+// tiles whose larger block falls in group g run (all their operands are
+// resident), and the region they complete -- rows [0, c0) x columns [c0, c1)
+// and rows [c0, c1) x columns [0, c1) -- goes D2H on the copy stream while
+// group g + 1 uploads and computes.  The egress (PCIe D2H of m^2 elements,
+// the floor of this call) then starts after 1/S of the upload instead of all
+// of it.
+int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,
+                          double epsilon, int include_diagonal, int out_kind, void* h_out, const DevInfo& info,
+                          int stages) {
+    const int64_t nw = (n_rows + 63) / 64;
+    const int64_t ld = mi_kmajor_ld(n_rows);
+    const int64_t m_pad = mi_kmajor_rows(n_cols);
+    const int tile = mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
+    int S = (int)(stages < T ? stages : T);
+    const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
+    // group boundaries in blocks: even (ingest_split 0), or doubling (1:
+    // T/2^(S-1), ..., T/4, T/2, T).  Doubling starts the egress after a small
+    // first upload and leaves half of the matrix to the last group, whose
+    // rows go down as one linear copy; even groups make 3/4 of it 2-D copies.
+    std::vector<int64_t> blk;
+    blk.push_back(0);
+    for (int g = 1; g <= S; ++g) {
+        const int64_t b = tuning().ingest_split ? (T >> (S - g)) : T * g / S;
+        if (b > blk.back()) blk.push_back(b);
+    }
+    if (blk.back() != T) blk.push_back(T);
+    S = (int)blk.size() - 1;
+    int rc;
+    if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
+    if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
+    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
+    if ((rc = ensure(&ws.out, &ws.out_cap, (size_t)n_cols * (size_t)n_cols * esz))) return rc;
+    // per-stage tile lists (banded order restricted to J in the group), one upload
+    const std::vector<int32_t> all = all_tiles(T, tile_band(), 0);
+    std::vector<int32_t> lists;
+    std::vector<int64_t> first(S + 1, 0);
+    for (int g = 0; g < S; ++g) {
+        first[g] = (int64_t)lists.size() / 2;
+        for (size_t k = 0; k < all.size(); k += 2)
+            if (all[k + 1] >= blk[g] && all[k + 1] < blk[g + 1]) {
+                lists.push_back(all[k]);
+                lists.push_back(all[k + 1]);
+            }
+    }
+    first[S] = (int64_t)lists.size() / 2;
+    if ((rc = ensure(&ws.tiles, &ws.tiles_cap, lists.size() * 4))) return rc;
+    MI_CUDA(cudaMemcpyAsync(ws.tiles, lists.data(), lists.size() * 4, cudaMemcpyHostToDevice, ws.stream));
+    for (int g = 0; g < S; ++g)
+        if (!ws.stage_ev[g]) MI_CUDA(cudaEventCreateWithFlags(&ws.stage_ev[g], cudaEventDisableTiming));
+    ColStat* cs = (ColStat*)ws.colstat;
+    long long* xl = xlogx_ptr(ws.colstat, n_rows, n_cols);
+    int2* br = blkrange_ptr(ws.colstat, n_rows, n_cols);
+    const bool fp4 = operand_fp4(n_rows);
+    MI_CUDA(launch_unpack_prep(n_rows, m_pad, cs, xl, br, fixr_ptr(ws.colstat, n_rows, n_cols), info.num_sms,
+                               ws.stream));
+    const size_t pitch = (size_t)n_cols * esz;
+    // Pageable words (the drop-in's numpy arrays) copy at ~10 GB/s through the
+    // driver's bounce buffer, one stage after another, which starved the
+    // pipeline (config 3: 14 ms of upload).  Stage them into a pinned buffer
+    // with host threads instead, group by group, so each group's H2D runs at
+    // link speed while the next group is being copied.
+    const uint64_t* src_words = h_words;
+    const bool stage_host = !host_is_pinned(h_words);
+    if (stage_host) {
+        const size_t need = (size_t)(n_cols * nw * 8);
+        if (ws.h_stage_cap < need) {
+            if (ws.h_stage) cudaFreeHost(ws.h_stage);
+            ws.h_stage = nullptr;
+            ws.h_stage_cap = 0;
+            MI_CUDA(cudaHostAlloc(&ws.h_stage, need, cudaHostAllocDefault));
+            ws.h_stage_cap = need;
+        }
+        src_words = (const uint64_t*)ws.h_stage;
+    }
+    const int copy_threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    // MI_B200_TIMELINE=1: per-stage event timeline on stderr (experiments only)
+    const bool tl_on = env_int("MI_B200_TIMELINE", 0) != 0;
+    std::vector<cudaEvent_t> tl;
+    auto mark = [&](cudaStream_t st) {
+        if (!tl_on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tl.push_back(e);
+    };
+    mark(ws.stream);
+    for (int g = 0; g < S; ++g) {
+        const int64_t c0 = std::min<int64_t>(blk[g] * tile, n_cols), c1 = std::min<int64_t>(blk[g + 1] * tile, n_cols);
+        if (stage_host)  // (the previous groups' H2D copies read other parts of the staging buffer)
+            parallel_memcpy((uint64_t*)ws.h_stage + c0 * nw, h_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
+                            copy_threads);
+        MI_CUDA(cudaMemcpyAsync((uint64_t*)ws.words + c0 * nw, src_words + c0 * nw, (size_t)((c1 - c0) * nw * 8),
+                                cudaMemcpyHostToDevice, ws.stream));
+        mark(ws.stream);  // H2D g done
+        const int64_t u1 = g == S - 1 ? m_pad : blk[g + 1] * tile;
+        MI_CUDA(launch_unpack_range((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
+                                    (int32_t*)ws.colsum, cs, xl ? br : nullptr, fp4, nullptr, tile, blk[g] * tile, u1,
+                                    info.num_sms, ws.stream));
+        if ((rc = launch_fused((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, epsilon, include_diagonal,
+                               out_kind, ws.out, n_cols, (const int32_t*)ws.tiles + 2 * first[g],
+                               first[g + 1] - first[g], nullptr, ws.stream)))
+            return rc;
+        MI_CUDA(cudaEventRecord(ws.stage_ev[g], ws.stream));
+        mark(ws.stream);  // compute g done
+        MI_CUDA(cudaStreamWaitEvent(ws.copy_stream, ws.stage_ev[g], 0));
+        mark(ws.copy_stream);  // D2H g may start
+        char* ho = (char*)h_out;
+        const char* dv = (const char*)ws.out;
+        if (c0 > 0 && c1 > c0)  // rows above the group, the group's columns
+            MI_CUDA(cudaMemcpy2DAsync(ho + c0 * esz, pitch, dv + c0 * esz, pitch, (size_t)(c1 - c0) * esz,
+                                      (size_t)c0, cudaMemcpyDeviceToHost, ws.copy_stream));
+        // the group's rows, columns [0, c1); one linear copy when they are whole
+        // rows (the last group): 2-D copies run at ~52 GB/s against ~57 GB/s
+        // linear on this link (tools/d2h_2d.py)
+        if (c1 > c0 && c1 == n_cols)
+            MI_CUDA(cudaMemcpyAsync(ho + c0 * pitch, dv + c0 * pitch, (size_t)(c1 - c0) * pitch,
+                                    cudaMemcpyDeviceToHost, ws.copy_stream));
+        else if (c1 > c0)
+            MI_CUDA(cudaMemcpy2DAsync(ho + c0 * pitch, pitch, dv + c0 * pitch, pitch, (size_t)c1 * esz,
+                                      (size_t)(c1 - c0), cudaMemcpyDeviceToHost, ws.copy_stream));
+        mark(ws.copy_stream);  // D2H g done
+    }
+    MI_CUDA(cudaStreamSynchronize(ws.copy_stream));
+    MI_CUDA(cudaStreamSynchronize(ws.stream));
+    if (tl_on) {
+        for (size_t k = 1; k < tl.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl[0], tl[k]);
+            static const char* what[4] = {"H2D done", "compute done", "D2H start", "D2H done"};
+            fprintf(stderr, "[timeline] stage %zu %-12s %8.3f ms\n", (k - 1) / 4, what[(k - 1) % 4], ms);
+        }
+        for (cudaEvent_t e : tl) cudaEventDestroy(e);
+    }
+    return MI_OK;
+}
+
+int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                        int include_diagonal, int out_kind, void* h_out, int device, bool packed) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
+    if (out_kind == MI_OUT_COUNTS) return fail(MI_ERR_DOMAIN, "use mi_gram_ones_host for counts");
+    if ((rc = check_padding(h_words, n_rows, n_cols))) return rc;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    const bool verbose = env_int("MI_B200_VERBOSE", 0) != 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto stamp = [&](const char* what) {
+        if (verbose)
+            fprintf(stderr, "[mi_all_pairs_host] %8.3f ms %s\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+    };
+    Workspace* ws;
+    DevInfo info;
+    if ((rc = workspace_for(device, &ws, &info))) return rc;
+    if (!packed && tuning().ingest > 0 && tiles_per_side(n_cols) > 1) {
+        rc = all_pairs_host_staged(*ws, h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out,
+                                   info, tuning().ingest);
+        stamp("done (staged)");
+        return rc;
+    }
+    int64_t ld, m_pad;
+    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    stamp("H2D + unpack enqueued");
+    const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
+    const size_t row_bytes = (size_t)n_cols * esz;
+    // byte offset of row r's first element in the output (full or packed upper triangle)
+    auto row_off = [&](int64_t r) -> size_t {
+        return packed ? (size_t)(r * n_cols - (r * (r - 1)) / 2) * esz : (size_t)r * row_bytes;
+    };
+    if ((rc = ensure(&ws->out, &ws->out_cap, row_off(n_cols)))) return rc;
+    // per-tile-row completion counters in pinned, mapped host memory
+    const int tile = mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
+    if (ws->row_done_cap < (size_t)T) {
+        if (ws->row_done_h) cudaFreeHost(ws->row_done_h);
+        ws->row_done_h = nullptr;
+        ws->row_done_cap = 0;
+        MI_CUDA(cudaHostAlloc((void**)&ws->row_done_h, (size_t)T * 4, cudaHostAllocMapped));
+        MI_CUDA(cudaHostGetDevicePointer((void**)&ws->row_done_d, ws->row_done_h, 0));
+        ws->row_done_cap = (size_t)T;
+        stamp("row counters allocated");
+    }
+    volatile unsigned int* done = ws->row_done_h;
+    for (int64_t I = 0; I < T; ++I) done[I] = 0;
+    // completion count of tile row I: +1 per CTA per tile (I, J), or per
+    // column slice of a split tail tile -- the same tile list and tail plan
+    // that run_fused launches
+    const unsigned cg = (unsigned)cta_group();
+    std::vector<unsigned> expect((size_t)T, 0u);
+    {
+        const std::vector<int32_t> tl = all_tiles(T, tile_band(), 1);
+        const int64_t nt = (int64_t)tl.size() / 2;
+        const TailPlan tp = tail_plan(nt, (int)cg, info.num_sms / (int)cg, (int)(mi_kmajor_ld(n_rows) / 128));
+        for (int64_t k = 0; k < nt; ++k) expect[(size_t)tl[2 * k]] += cg * (k >= tp.n_full ? (unsigned)tp.epi : 1u);
+    }
+    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out,
+                        packed ? MI_PACKED_UPPER : n_cols, info, ws->row_done_d)))
+        return rc;
+    stamp("fused kernel enqueued");
+    // Stream finished rows to the host while the GEMM continues: rows of tile
+    // row b are final once every tile row I <= b is complete (its own tiles
+    // and all mirrors landing in it), so copy the completed prefix.
+    // At most two copies in flight: while the link is busy the finished rows
+    // accumulate, so chunks grow (a handful of copies in all; each extra copy
+    // costs ~25 us of engine time, tools/d2h_streams.py), yet the queued one
+    // keeps the copy engine from idling between them.
+    const int64_t min_chunk_rows = (int64_t)((16u << 20) / row_bytes) + 1;  // (packed: rows shrink; fine)
+    int64_t copied = 0, I = 0;
+    bool kernel_done = false;
+    if (!ws->copy_ev[0]) {
+        MI_CUDA(cudaEventCreateWithFlags(&ws->copy_ev[0], cudaEventDisableTiming));
+        MI_CUDA(cudaEventCreateWithFlags(&ws->copy_ev[1], cudaEventDisableTiming));
+    }
+    int issued = 0;
+    auto in_flight = [&]() {
+        int n = 0;
+        for (int k = issued - 2 < 0 ? 0 : issued - 2; k < issued; ++k)
+            if (cudaEventQuery(ws->copy_ev[k & 1]) == cudaErrorNotReady) ++n;
+        return n;
+    };
+    while (copied < n_cols) {
+        while (I < T && done[I] >= expect[(size_t)I]) ++I;
+        int64_t final_rows = I * tile < n_cols ? I * tile : n_cols;
+        if (kernel_done) final_rows = n_cols;
+        if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols) &&
+            (kernel_done || in_flight() < 2)) {
+            MI_CUDA(cudaMemcpyAsync((char*)h_out + row_off(copied), (char*)ws->out + row_off(copied),
+                                    row_off(final_rows) - row_off(copied), cudaMemcpyDeviceToHost, ws->copy_stream));
+            MI_CUDA(cudaEventRecord(ws->copy_ev[issued & 1], ws->copy_stream));
+            ++issued;
+            if (verbose) {
+                char msg[96];
+                snprintf(msg, sizeof(msg), "D2H rows [%lld, %lld) issued", (long long)copied, (long long)final_rows);
+                stamp(msg);
+            }
+            copied = final_rows;
+            continue;
+        }
+        const cudaError_t q = cudaStreamQuery(ws->stream);
+        if (q == cudaSuccess) {
+            kernel_done = true;  // everything is final now
+        } else if (q != cudaErrorNotReady) {
+            cudaStreamSynchronize(ws->copy_stream);
+            return cuda_fail(q, "fused kernel");
+        } else {
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+    MI_CUDA(cudaStreamSynchronize(ws->copy_stream));
+    MI_CUDA(cudaStreamSynchronize(ws->stream));
+    stamp("done");
+    return MI_OK;
+}
+
+int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, int64_t* h_out, int device) {
+    if (n_cols < 1 || n_words < 1) return fail(MI_ERR_DIMENSION, "words must be a non-empty (m, nw) array");
+    const int64_t n_rows = n_words * 64;  // padding bits are zero, so they add nothing
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    DevInfo info;
+    int rc;
+    if ((rc = workspace_for(device, &ws, &info))) return rc;
+    int64_t ld, m_pad;
+    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * 4;
+    if ((rc = ensure(&ws->out, &ws->out_cap, out_bytes))) return rc;
+    if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, MI_MODE_EXACT, 1e-12, 1, MI_OUT_COUNTS, ws->out, n_cols,
+                        info)))
+        return rc;
+    std::vector<int32_t> tmp((size_t)n_cols * (size_t)n_cols);
+    MI_CUDA(cudaMemcpyAsync(tmp.data(), ws->out, out_bytes, cudaMemcpyDeviceToHost, ws->stream));
+    MI_CUDA(cudaStreamSynchronize(ws->stream));
+    for (size_t k = 0; k < tmp.size(); ++k) h_out[k] = tmp[k];
+    return MI_OK;
+}
+
+int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, uint64_t* h_out, int device) {
+    if (n_cols < 1 || n_words < 1) return fail(MI_ERR_DIMENSION, "words must be a non-empty (m, nw) array");
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace* ws;
+    DevInfo info;
+    int rc;
+    if ((rc = workspace_for(device, &ws, &info))) return rc;
+    int64_t ld, m_pad;
+    if ((rc = stage_inputs(*ws, h_words, n_words * 64, n_cols, &ld, &m_pad, info))) return rc;
+    std::vector<int32_t> tmp((size_t)n_cols);
+    MI_CUDA(cudaMemcpyAsync(tmp.data(), ws->colsum, (size_t)n_cols * 4, cudaMemcpyDeviceToHost, ws->stream));
+    MI_CUDA(cudaStreamSynchronize(ws->stream));
+    for (int64_t k = 0; k < n_cols; ++k) h_out[k] = (uint64_t)tmp[k];
+    return MI_OK;
+}
+
+// ---------------------------------------------------------------- sharded egress
+
+int mi_host_register(void* h_ptr, int64_t bytes) {
+    if (!h_ptr || bytes < 1) return fail(MI_ERR_DOMAIN, "bad host range");
+    MI_CUDA(cudaHostRegister(h_ptr, (size_t)bytes, cudaHostRegisterPortable));
+    return MI_OK;
+}
+
+int mi_host_unregister(void* h_ptr) {
+    if (!h_ptr) return fail(MI_ERR_DOMAIN, "null host pointer");
+    MI_CUDA(cudaHostUnregister(h_ptr));
+    return MI_OK;
+}
+
+// Tiles and their mirrors, device -> host, as few 2-D copies as possible: runs
+// of consecutive J in a tile row merge, then identical runs in consecutive tile
+// rows (an 8-rank column-group share is one or two rectangles).
+int mi_copy_tiles_to_host(const void* d_out, int64_t ld_out, int64_t n_cols, int esz, const int32_t* h_tiles,
+                          int64_t n_tiles, void* h_dst, int64_t ld_dst, void* stream) {
+    if (!d_out || !h_dst || (n_tiles > 0 && !h_tiles)) return fail(MI_ERR_DOMAIN, "null argument");
+    if (esz != 4 && esz != 8) return fail(MI_ERR_DOMAIN, "esz must be 4 or 8");
+    if (ld_out < n_cols || ld_dst < n_cols) return fail(MI_ERR_DIMENSION, "pitch < n_cols");
+    const int64_t t = mi_tile_size();
+    const int64_t T = tiles_per_side(n_cols);
+    std::vector<std::pair<int32_t, int32_t>> v;
+    v.reserve((size_t)n_tiles);
+    for (int64_t k = 0; k < n_tiles; ++k) {
+        const int32_t I = h_tiles[2 * k], J = h_tiles[2 * k + 1];
+        if (I < 0 || J < 0 || I >= T || J >= T) return fail(MI_ERR_DIMENSION, "tile (%d, %d) outside %lld", I, J, (long long)T);
+        v.push_back({I, J});
+    }
+    std::sort(v.begin(), v.end());
+    struct Run { int32_t I, J0, J1; };  // tile row I, tile columns [J0, J1)
+    std::vector<Run> runs;
+    for (size_t k = 0; k < v.size();) {
+        size_t e = k + 1;
+        while (e < v.size() && v[e].first == v[k].first && v[e].second == v[e - 1].second + 1) ++e;
+        runs.push_back({v[k].first, v[k].second, v[e - 1].second + 1});
+        k = e;
+    }
+    struct Rect { int32_t I0, I1, J0, J1; };
+    std::vector<Rect> rects;
+    for (const Run& r : runs) {
+        if (!rects.empty() && rects.back().I1 == r.I && rects.back().J0 == r.J0 && rects.back().J1 == r.J1)
+            rects.back().I1 = r.I + 1;
+        else
+            rects.push_back({r.I, r.I + 1, r.J0, r.J1});
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    auto copy = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+        r1 = r1 < n_cols ? r1 : n_cols;
+        c1 = c1 < n_cols ? c1 : n_cols;
+        if (r0 >= r1 || c0 >= c1) return MI_OK;
+        MI_CUDA(cudaMemcpy2DAsync((char*)h_dst + (r0 * ld_dst + c0) * esz, (size_t)(ld_dst * esz),
+                                  (const char*)d_out + (r0 * ld_out + c0) * esz, (size_t)(ld_out * esz),
+                                  (size_t)((c1 - c0) * esz), (size_t)(r1 - r0), cudaMemcpyDeviceToHost, st));
+        return MI_OK;
+    };
+    int rc;
+    for (const Rect& q : rects) {
+        if ((rc = copy(q.I0 * t, q.I1 * t, q.J0 * t, q.J1 * t))) return rc;  // tiles
+        if ((rc = copy(q.J0 * t, q.J1 * t, q.I0 * t, q.I1 * t))) return rc;  // mirrors
+    }
+    return MI_OK;
+}
+
+void mi_release_workspace(void) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto& w : g_ws) release(w);
+}
+
+}  // extern "C"

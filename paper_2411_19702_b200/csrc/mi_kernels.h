@@ -115,6 +115,11 @@ cudaError_t launch_column_order(const uint64_t* words, int64_t n_rows, int64_t m
 cudaError_t launch_unpermute(const void* in, int64_t ld_in, void* out, int64_t ld_out, int64_t m, int esz,
                              const int32_t* inv, int num_sms, int smem_bytes, int ctas_per_sm, cudaStream_t stream);
 
+// Tensor-peak probe (probe.cu): reps x 16 back-to-back 2-SM MMAs per SM pair;
+// d_cycles[pair] = clock64 cycles of the issuing thread.
+cudaError_t launch_tensor_peak(bool fp4, int reps, int num_sms, long long* d_cycles, cudaStream_t stream);
+double tensor_peak_macs_per_pair(bool fp4, int reps);
+
 cudaError_t launch_generate_words(uint64_t* words, int64_t n_rows, int64_t m, uint64_t seed,
                                   const uint64_t* col_threshold, const uint8_t* col_kind,
                                   const int32_t* col_src, uint64_t flip_threshold,
