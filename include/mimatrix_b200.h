@@ -25,7 +25,8 @@
  * ld_out = MI_PACKED_UPPER (upper-triangle egress), mi_tile_list /
  * mi_rank_blocks / mi_unpack_colsum_blocks (multi-GPU shares),
  * mi_column_order / mi_unpack_colsum_ordered / mi_unpermute (column-sum order),
- * mi_host_register / mi_copy_tiles_to_host (sharded host egress), the
+ * mi_host_register / mi_copy_tiles_to_host / mi_scatter_tiles and
+ * ld_out = MI_TILE_MAJOR (sharded output and its gather), the
  * layout queries and the tuning knobs.
  * Error codes mirror the reference's exception classes (errors.py:8-25).
  */
@@ -52,6 +53,12 @@ extern "C" {
 /* ld_out value selecting the packed upper-triangle output: element (i, j >= i)
  * at i*m - i*(i-1)/2 + (j - i), m(m+1)/2 elements, nothing mirrored. */
 #define MI_PACKED_UPPER 0
+/* ld_out value selecting the tile-major (sharded) output of mi_gram_mi: tile k
+ * of the launch's list is stored at d_out + k * T * T elements (T =
+ * mi_tile_size(), row pitch T, element (i, j) of tile (I, J) at row i - I*T,
+ * column j - J*T), without its mirror.  mi_scatter_tiles places such shards
+ * (tiles and mirrors) into a full matrix on a device or in pinned host memory. */
+#define MI_TILE_MAJOR (-1)
 
 /* engine modes (engine.py:28, EngineConfig.mode) */
 #define MI_MODE_EXACT 0
@@ -124,7 +131,8 @@ int mi_unpack_colsum_range(const uint64_t* d_words, int64_t n_rows, int64_t n_co
                            int64_t c_begin, int64_t c_end, void* stream);
 /* Fused G11 + MI over the listed upper-triangle tiles; writes each tile and
  * its mirror into d_out (row-major, pitch ld_out elements), or with ld_out =
- * MI_PACKED_UPPER only the elements j >= i, packed (see above). */
+ * MI_PACKED_UPPER only the elements j >= i, packed, or with ld_out =
+ * MI_TILE_MAJOR each tile alone into its slot (see above). */
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
                int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
                int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
@@ -180,7 +188,8 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
                         int device);
 /* ---- egress of a sharded result into one host matrix ----
  * Pin host memory allocated elsewhere (e.g. a POSIX shared-memory segment
- * that every rank on the node maps) for asynchronous copies. */
+ * that every rank on the node maps) for asynchronous copies and for device
+ * kernels writing it directly (mapped, portable). */
 int mi_host_register(void* h_ptr, int64_t bytes);
 int mi_host_unregister(void* h_ptr);
 /* Copy the listed tiles (h_tiles: host (I, J) pairs as from mi_tile_list) and
@@ -190,6 +199,15 @@ int mi_host_unregister(void* h_ptr);
  * PCIe link. */
 int mi_copy_tiles_to_host(const void* d_out, int64_t ld_out, int64_t n_cols, int esz, const int32_t* h_tiles,
                           int64_t n_tiles, void* h_dst, int64_t ld_dst, void* stream);
+/* Tile-major shards (mi_gram_mi with MI_TILE_MAJOR) -> a full row-major matrix:
+ * tile k of d_tiles (device (I, J) pairs) from d_src + k*T*T into rows I*T..,
+ * columns J*T.. of d_dst (pitch ld_dst elements, esz 4 or 8 bytes), and with
+ * `mirror` its transpose at (J, I) as well (off-diagonal tiles).  d_dst may be
+ * device memory or pinned / mi_host_register'ed host memory (written over
+ * PCIe by the kernel, zero-copy).  The multi-GPU gather: each rank places its
+ * own shard. */
+int mi_scatter_tiles(const void* d_src, const int32_t* d_tiles, int64_t n_tiles, int64_t n_cols, int esz, void* d_dst,
+                     int64_t ld_dst, int mirror, void* stream);
 
 /* ---- ingest: the BMI1 packed container (io.py:1-16, read_bmi io.py:92-116) ----
  * "BMI1", n_rows (u64 LE), n_cols (u64 LE), then n_cols columns of

@@ -34,6 +34,7 @@ MI_OUT_COUNTS = 0
 MI_OUT_F64 = 1
 MI_OUT_F32 = 2
 MI_PACKED_UPPER = 0  # ld_out selecting the packed upper-triangle output
+MI_TILE_MAJOR = -1  # ld_out selecting the tile-major (sharded) output
 
 _ERRORS = {
     MI_ERR_DIMENSION: DimensionError,
@@ -79,6 +80,7 @@ SIGNATURES = {
     "mi_host_register": (_int, [_vp, _i64]),
     "mi_host_unregister": (_int, [_vp]),
     "mi_copy_tiles_to_host": (_int, [_vp, _i64, _i64, _int, _vp, _i64, _vp, _i64, _vp]),
+    "mi_scatter_tiles": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _i64, _int, _vp]),
     "mi_bmi_header": (_int, [ctypes.c_char_p, _vp, _vp]),
     "mi_bmi_load": (_int, [ctypes.c_char_p, _vp, _i64, _i64, _vp]),
     "mi_set_tuning": (_int, [ctypes.c_char_p, _int]),

@@ -53,7 +53,8 @@ std::vector<int32_t> all_tiles(int64_t T, int band, int first) {
 }
 
 // A rank's tiles.  Round robin over the banded order (every rank touches
-// nearly every column block), except for 8 ranks ("shard" knob, T >= 8): the
+// nearly every column block), except for 4 ranks (below: each rank holds 3 of
+// 4 column groups) and 8 ranks ("shard" knob, T >= 8): the
 // column blocks form 4 groups; ranks 0-5 take the 6 off-diagonal group pairs
 // (g, h), ranks 6 and 7 two diagonal groups each ((0,0)+(3,3), (1,1)+(2,2)).
 // Every rank then reads -- and unpacks -- only 2 of the 4 groups (half of X),
@@ -109,6 +110,58 @@ std::vector<int32_t> rank_tiles(int64_t T, int rank, int world, int band) {
             }
         }
         return share[rank];
+    }
+    if (world == 4 && T >= 16 && tuning().shard) {
+        // 4 column groups; rank r holds every group but r (3/4 of X).  Every
+        // group pair (g, h) lies in the two or three ranks that hold both;
+        // tiles go, in the banded order, to the least-loaded of those, so the
+        // shares differ by at most a tile or two and each rank unpacks 3/4 of X
+        // instead of all of it.
+        auto group = [&](int64_t b) { return (int)((b * 4) / T); };
+        // each group pair's tiles go round robin over the ranks that hold
+        // both groups (2 for an off-diagonal pair, 3 for a diagonal one), so
+        // every rank gets half of three off-diagonal pairs and a third of three
+        // diagonal ones; the rank's list keeps the banded order
+        std::vector<int8_t> owner((size_t)total, -1);
+        int cnt[4][4] = {};
+        for (int64_t k = 0; k < total; ++k) {
+            const int gi = group(all[2 * k]), gj = group(all[2 * k + 1]);
+            int elig[3], ne = 0;
+            for (int r = 0; r < 4; ++r)
+                if (r != gi && r != gj) elig[ne++] = r;
+            owner[(size_t)k] = (int8_t)elig[cnt[gi][gj]++ % ne];
+        }
+        // unequal group sizes (T % 4 != 0) leave a small imbalance: move tiles,
+        // from the end of the order, off the most loaded rank to the least
+        // loaded rank that also holds both of their groups
+        int64_t load[4] = {0, 0, 0, 0};
+        for (int64_t k = 0; k < total; ++k) ++load[owner[(size_t)k]];
+        for (int64_t moves = 0; moves < total; ++moves) {
+            int hi = 0;
+            for (int r = 1; r < 4; ++r)
+                if (load[r] > load[hi]) hi = r;
+            bool moved = false;
+            for (int64_t k = total - 1; k >= 0 && !moved; --k) {
+                if (owner[(size_t)k] != hi) continue;
+                const int gi = group(all[2 * k]), gj = group(all[2 * k + 1]);
+                int lo = -1;
+                for (int r = 0; r < 4; ++r)
+                    if (r != gi && r != gj && r != hi && load[r] + 1 < load[hi] && (lo < 0 || load[r] < load[lo]))
+                        lo = r;
+                if (lo < 0) continue;
+                owner[(size_t)k] = (int8_t)lo;
+                --load[hi];
+                ++load[lo];
+                moved = true;
+            }
+            if (!moved) break;
+        }
+        for (int64_t k = 0; k < total; ++k)
+            if (owner[(size_t)k] == rank) {
+                v.push_back(all[2 * k]);
+                v.push_back(all[2 * k + 1]);
+            }
+        return v;
     }
     for (int64_t g = rank; g < total; g += world) {
         v.push_back(all[2 * g]);

@@ -275,7 +275,7 @@ __device__ __forceinline__ void store16(const T (&v)[16], int i, int j0, const G
     // 2) mirror tile: row j, column i (coalesced across the warp)
     const bool hint = (p.debug & 8) != 0;
     const uint64_t pol = hint ? l2_policy_evict_first() : 0ull;
-    if (!DIAG && !(p.debug & 2)) {
+    if (!DIAG && !p.tile_major && !(p.debug & 2)) {
         if (hint) {
 #pragma unroll
             for (int k = 0; k < 16; ++k)
@@ -845,6 +845,12 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             }
             const RowMarg A = row_marg(Arow, eN, dN);
             const bool row_ok = i < m;
+            // output base: the matrix, or (tile-major shards) slot t of TS x TS
+            // rows, addressed with the tile's global (i, j) so the stores are shared
+            T* const o = p.tile_major ? out + ((int64_t)t * C::TS - (int64_t)tile.x * C::TS) * C::TS -
+                                            (int64_t)tile.y * C::TS
+                                      : out;
+            const int64_t ldd = p.tile_major ? (int64_t)C::TS : ld;
             mbar_wait(tfull_bar(acc), aph);
             tc_fence_after();
             if (tracer && it < 64) p.trace[it * 4 + 2] = clock64();
@@ -913,41 +919,41 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                         }
                     }
                 }
-                const bool vec_ok = ((reinterpret_cast<uintptr_t>(out + (int64_t)i * ld + j0) & (2 * sizeof(T) - 1)) == 0);
+                const bool vec_ok = ((reinterpret_cast<uintptr_t>(o + (int64_t)i * ldd + j0) & (2 * sizeof(T) - 1)) == 0);
                 if (use_f32) {
                     if constexpr (MODE == MI_MODE_EXACT && OUT == MI_OUT_F32) {
                         constexpr bool RAW = FP4 && TAIL != 2;
                         if (diag)
-                            epilogue16_f32<true, RAW>(r, i, j0, Af, colsf + c0 + col0, p, dNf, rNf, out, ld, row_ok,
+                            epilogue16_f32<true, RAW>(r, i, j0, Af, colsf + c0 + col0, p, dNf, rNf, o, ldd, row_ok,
                                                       vec_ok);
                         else
-                            epilogue16_f32<false, RAW>(r, i, j0, Af, colsf + c0 + col0, p, dNf, rNf, out, ld, row_ok,
+                            epilogue16_f32<false, RAW>(r, i, j0, Af, colsf + c0 + col0, p, dNf, rNf, o, ldd, row_ok,
                                                        vec_ok);
                     }
                 } else if (use_table) {
                     if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
                         if (diag)
                             epilogue16<OUT, MODE, true, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
-                                                                     dN, rN, tab, out, ld, row_ok, vec_ok);
+                                                                     dN, rN, tab, o, ldd, row_ok, vec_ok);
                         else
                             epilogue16<OUT, MODE, false, true, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
-                                                                      dN, rN, tab, out, ld, row_ok, vec_ok);
+                                                                      dN, rN, tab, o, ldd, row_ok, vec_ok);
                     }
                 } else if (use_hybrid) {
                     if constexpr (MODE == MI_MODE_EXACT && OUT != MI_OUT_COUNTS) {
                         if (diag)
                             epilogue16<OUT, MODE, true, true, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
-                                                                    dN, rN, tab, out, ld, row_ok, vec_ok);
+                                                                    dN, rN, tab, o, ldd, row_ok, vec_ok);
                         else
                             epilogue16<OUT, MODE, false, true, true>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN,
-                                                                     dN, rN, tab, out, ld, row_ok, vec_ok);
+                                                                     dN, rN, tab, o, ldd, row_ok, vec_ok);
                     }
                 } else if (diag) {
                     epilogue16<OUT, MODE, true, false, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN,
-                                                              tab, out, ld, row_ok, vec_ok);
+                                                              tab, o, ldd, row_ok, vec_ok);
                 } else {
                     epilogue16<OUT, MODE, false, false, false>(r, i, j0, A, AQ, cols + c0 + col0, Arow, p, eN, fN, dN, rN,
-                                                               tab, out, ld, row_ok, vec_ok);
+                                                               tab, o, ldd, row_ok, vec_ok);
                 }
             }
             // hand the accumulator back to the MMA warp (EVAC: done above)

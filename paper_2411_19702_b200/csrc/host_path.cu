@@ -40,6 +40,8 @@ struct Workspace {
     void* tiles = nullptr; size_t tiles_cap = 0;
     void* out = nullptr; size_t out_cap = 0;
     void* h_stage = nullptr; size_t h_stage_cap = 0;  // pinned staging of pageable host words
+    void* h_egress = nullptr; size_t h_egress_cap = 0;  // pinned staging of a pageable host output
+    std::vector<cudaEvent_t> piece_ev;  // staged path: one per D2H piece (pageable output)
     cudaStream_t copy_stream = nullptr;   // D2H of finished row bands
     cudaEvent_t copy_ev[2] = {nullptr, nullptr};  // the last two D2H copies
     cudaEvent_t stage_ev[kMaxIngestStages] = {};  // staged path: stage g's tiles are stored
@@ -77,6 +79,11 @@ void release(Workspace& w) {
         if (e) cudaEventDestroy(e), e = nullptr;
     if (w.row_done_h) cudaFreeHost(w.row_done_h), w.row_done_h = nullptr, w.row_done_d = nullptr;
     if (w.h_stage) cudaFreeHost(w.h_stage), w.h_stage = nullptr;
+    if (w.h_egress) cudaFreeHost(w.h_egress), w.h_egress = nullptr;
+    w.h_egress_cap = 0;
+    for (auto& e : w.piece_ev)
+        if (e) cudaEventDestroy(e);
+    w.piece_ev.clear();
     w.h_stage_cap = 0;
     w.row_done_cap = 0;
     w.device = -1;
@@ -95,15 +102,16 @@ bool host_is_pinned(const void* h) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
-// memcpy with up to `threads` host threads (pageable -> pinned staging): one
-// thread reaches ~10 GB/s, well short of the link's ~55.  The workers are a
-// small persistent pool (created on first use, never torn down: spawning 8
-// threads per group cost ~1 ms a call); calls are serialised by g_ws_mu.
+// Host copy threads between pageable user memory and the pinned staging
+// buffers: one thread reaches ~10 GB/s, well short of the link's ~55.  The
+// workers are a small persistent pool (created on first use, never torn
+// down: spawning 8 threads per group cost ~1 ms a call); one batch at a time.
 struct CopyPool {
     std::mutex mu;
     std::condition_variable cv, done_cv;
     std::vector<std::thread> workers;
-    struct Job { char* dst; const char* src; size_t n; };
+    // rows x width bytes, row r from src + r spitch to dst + r dpitch
+    struct Job { char* dst; const char* src; size_t width, rows, dpitch, spitch; };
     std::vector<Job> jobs;
     size_t next = 0, pending = 0;
     void ensure(int n) {
@@ -116,7 +124,10 @@ struct CopyPool {
                         cv.wait(lk, [this] { return next < jobs.size(); });
                         j = jobs[next++];
                     }
-                    memcpy(j.dst, j.src, j.n);
+                    if (j.rows == 1 || (j.dpitch == j.width && j.spitch == j.width))
+                        memcpy(j.dst, j.src, j.width * j.rows);
+                    else
+                        for (size_t r = 0; r < j.rows; ++r) memcpy(j.dst + r * j.dpitch, j.src + r * j.spitch, j.width);
                     std::lock_guard<std::mutex> lk(mu);
                     if (--pending == 0) done_cv.notify_all();
                 }
@@ -129,31 +140,43 @@ CopyPool& copy_pool() {
     static CopyPool* p = new CopyPool();  // leaked on purpose: detached workers outlive static destruction
     return *p;
 }
+std::mutex g_copy_mu;  // one batch at a time (callers on several device threads take turns)
 
-void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+// 2-D copy (rows of `width` bytes) split over up to `threads` host threads.
+void parallel_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                      int threads) {
+    if (!rows || !width) return;
+    const size_t bytes = width * rows;
     const size_t min_chunk = (size_t)4 << 20;
-    const int t = (int)std::min<size_t>((size_t)threads, (bytes + min_chunk - 1) / min_chunk);
+    const int t = (int)std::min<size_t>(std::min<size_t>((size_t)threads, rows), (bytes + min_chunk - 1) / min_chunk);
     if (t <= 1) {
-        memcpy(dst, src, bytes);
+        for (size_t r = 0; r < rows; ++r) memcpy((char*)dst + r * dpitch, (const char*)src + r * spitch, width);
         return;
     }
+    std::lock_guard<std::mutex> serial(g_copy_mu);
     CopyPool& pool = copy_pool();
     pool.ensure(t);
-    const size_t chunk = (bytes + t - 1) / t;
+    const size_t per = (rows + t - 1) / t;
     {
         std::lock_guard<std::mutex> lk(pool.mu);
         pool.jobs.clear();
         pool.next = 0;
-        for (int i = 0; i < t; ++i) {
-            const size_t o = (size_t)i * chunk;
-            if (o >= bytes) break;
-            pool.jobs.push_back({(char*)dst + o, (const char*)src + o, std::min(chunk, bytes - o)});
-        }
+        for (size_t r0 = 0; r0 < rows; r0 += per)
+            pool.jobs.push_back({(char*)dst + r0 * dpitch, (const char*)src + r0 * spitch, width,
+                                 std::min(per, rows - r0), dpitch, spitch});
         pool.pending = pool.jobs.size();
     }
     pool.cv.notify_all();
     std::unique_lock<std::mutex> lk(pool.mu);
     pool.done_cv.wait(lk, [&] { return pool.pending == 0; });
+}
+
+// memcpy with up to `threads` host threads.
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    const size_t chunk = (size_t)1 << 20;  // as 1 MB rows, split over the threads
+    const size_t rows = bytes / chunk;
+    if (rows) parallel_copy_2d(dst, chunk, src, chunk, chunk, rows, threads);
+    if (bytes % chunk) memcpy((char*)dst + rows * chunk, (const char*)src + rows * chunk, bytes % chunk);
 }
 
 // H2D of host words into ws.words on ws.stream.  Pageable words (numpy
@@ -182,6 +205,23 @@ int upload_words(Workspace& ws, const uint64_t* h_words, int64_t n_cols, int64_t
         MI_CUDA(cudaMemcpyAsync((char*)ws.words + off, (char*)ws.h_stage + off, len, cudaMemcpyHostToDevice,
                                 ws.stream));
     }
+    return MI_OK;
+}
+
+// Pageable host outputs (the drop-in's fresh numpy array) are filled through
+// a cached pinned egress buffer of the output's size: the copy engine writes
+// it at link speed and host threads copy each finished piece out while the
+// next pieces are still in flight (the driver's own pageable D2H runs at
+// ~10 GB/s).  Grow-only; released by mi_release_workspace.
+int egress_buffer(Workspace& ws, size_t bytes, void** out) {
+    if (ws.h_egress_cap < bytes) {
+        if (ws.h_egress) cudaFreeHost(ws.h_egress);
+        ws.h_egress = nullptr;
+        ws.h_egress_cap = 0;
+        MI_CUDA(cudaHostAlloc(&ws.h_egress, bytes, cudaHostAllocDefault));
+        ws.h_egress_cap = bytes;
+    }
+    *out = ws.h_egress;
     return MI_OK;
 }
 
@@ -333,6 +373,28 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
         src_words = (const uint64_t*)ws.h_stage;
     }
     const int copy_threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    // pageable output: D2H into the pinned egress buffer, pieces copied out below
+    const bool stage_out = !host_is_pinned(h_out);
+    char* d2h_dst = (char*)h_out;
+    if (stage_out) {
+        void* eb = nullptr;
+        if ((rc = egress_buffer(ws, (size_t)n_cols * (size_t)n_cols * esz, &eb))) return rc;
+        d2h_dst = (char*)eb;
+    }
+    struct Piece { int64_t r0, rows, c0, cols; };
+    std::vector<Piece> pieces;
+    auto piece_done = [&](const Piece& pc) -> int {  // record the piece's completion on the copy stream
+        if (!stage_out) return MI_OK;
+        const size_t k = pieces.size();
+        if (ws.piece_ev.size() <= k) {
+            cudaEvent_t e;
+            MI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ws.piece_ev.push_back(e);
+        }
+        MI_CUDA(cudaEventRecord(ws.piece_ev[k], ws.copy_stream));
+        pieces.push_back(pc);
+        return MI_OK;
+    };
     // MI_B200_TIMELINE=1: per-stage event timeline on stderr (experiments only)
     const bool tl_on = env_int("MI_B200_TIMELINE", 0) != 0;
     std::vector<cudaEvent_t> tl;
@@ -364,21 +426,40 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
         mark(ws.stream);  // compute g done
         MI_CUDA(cudaStreamWaitEvent(ws.copy_stream, ws.stage_ev[g], 0));
         mark(ws.copy_stream);  // D2H g may start
-        char* ho = (char*)h_out;
+        char* ho = d2h_dst;
         const char* dv = (const char*)ws.out;
-        if (c0 > 0 && c1 > c0)  // rows above the group, the group's columns
+        if (c0 > 0 && c1 > c0) {  // rows above the group, the group's columns
             MI_CUDA(cudaMemcpy2DAsync(ho + c0 * esz, pitch, dv + c0 * esz, pitch, (size_t)(c1 - c0) * esz,
                                       (size_t)c0, cudaMemcpyDeviceToHost, ws.copy_stream));
+            if ((rc = piece_done({0, c0, c0, c1 - c0}))) return rc;
+        }
         // the group's rows, columns [0, c1); one linear copy when they are whole
         // rows (the last group): 2-D copies run at ~52 GB/s against ~57 GB/s
-        // linear on this link (tools/d2h_2d.py)
-        if (c1 > c0 && c1 == n_cols)
-            MI_CUDA(cudaMemcpyAsync(ho + c0 * pitch, dv + c0 * pitch, (size_t)(c1 - c0) * pitch,
-                                    cudaMemcpyDeviceToHost, ws.copy_stream));
-        else if (c1 > c0)
+        // linear on this link (tools/d2h_2d.py).  With a pageable output the
+        // last rows go in 4 pieces, so the host copies trail the link closely.
+        if (c1 > c0 && c1 == n_cols) {
+            const int64_t parts = stage_out ? std::min<int64_t>(4, c1 - c0) : 1;
+            for (int64_t q = 0; q < parts; ++q) {
+                const int64_t a = c0 + (c1 - c0) * q / parts, b = c0 + (c1 - c0) * (q + 1) / parts;
+                if (b <= a) continue;
+                MI_CUDA(cudaMemcpyAsync(ho + a * pitch, dv + a * pitch, (size_t)(b - a) * pitch,
+                                        cudaMemcpyDeviceToHost, ws.copy_stream));
+                if ((rc = piece_done({a, b - a, 0, n_cols}))) return rc;
+            }
+        } else if (c1 > c0) {
             MI_CUDA(cudaMemcpy2DAsync(ho + c0 * pitch, pitch, dv + c0 * pitch, pitch, (size_t)c1 * esz,
                                       (size_t)(c1 - c0), cudaMemcpyDeviceToHost, ws.copy_stream));
+            if ((rc = piece_done({c0, c1 - c0, 0, c1}))) return rc;
+        }
         mark(ws.copy_stream);  // D2H g done
+    }
+    // pageable output: copy each piece out as soon as its D2H has landed
+    for (size_t k = 0; k < pieces.size(); ++k) {
+        MI_CUDA(cudaEventSynchronize(ws.piece_ev[k]));
+        const Piece& pc = pieces[k];
+        const size_t off = ((size_t)pc.r0 * (size_t)n_cols + (size_t)pc.c0) * esz;
+        parallel_copy_2d((char*)h_out + off, pitch, d2h_dst + off, pitch, (size_t)pc.cols * esz, (size_t)pc.rows,
+                         copy_threads);
     }
     MI_CUDA(cudaStreamSynchronize(ws.copy_stream));
     MI_CUDA(cudaStreamSynchronize(ws.stream));
@@ -428,6 +509,14 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
         return packed ? (size_t)(r * n_cols - (r * (r - 1)) / 2) * esz : (size_t)r * row_bytes;
     };
     if ((rc = ensure(&ws->out, &ws->out_cap, row_off(n_cols)))) return rc;
+    // pageable output: D2H into the pinned egress buffer, one host copy at the end
+    const bool stage_out = !host_is_pinned(h_out);
+    char* d2h_dst = (char*)h_out;
+    if (stage_out) {
+        void* eb = nullptr;
+        if ((rc = egress_buffer(*ws, row_off(n_cols), &eb))) return rc;
+        d2h_dst = (char*)eb;
+    }
     // per-tile-row completion counters in pinned, mapped host memory
     const int tile = mi_tile_size();
     const int64_t T = tiles_per_side(n_cols);
@@ -484,7 +573,7 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
         if (kernel_done) final_rows = n_cols;
         if (final_rows > copied && (final_rows - copied >= min_chunk_rows || final_rows == n_cols) &&
             (kernel_done || in_flight() < 2)) {
-            MI_CUDA(cudaMemcpyAsync((char*)h_out + row_off(copied), (char*)ws->out + row_off(copied),
+            MI_CUDA(cudaMemcpyAsync(d2h_dst + row_off(copied), (char*)ws->out + row_off(copied),
                                     row_off(final_rows) - row_off(copied), cudaMemcpyDeviceToHost, ws->copy_stream));
             MI_CUDA(cudaEventRecord(ws->copy_ev[issued & 1], ws->copy_stream));
             ++issued;
@@ -508,6 +597,8 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
     }
     MI_CUDA(cudaStreamSynchronize(ws->copy_stream));
     MI_CUDA(cudaStreamSynchronize(ws->stream));
+    if (stage_out)
+        parallel_memcpy(h_out, d2h_dst, row_off(n_cols), std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8))));
     stamp("done");
     return MI_OK;
 }
@@ -554,7 +645,7 @@ int mi_column_sums_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words
 
 int mi_host_register(void* h_ptr, int64_t bytes) {
     if (!h_ptr || bytes < 1) return fail(MI_ERR_DOMAIN, "bad host range");
-    MI_CUDA(cudaHostRegister(h_ptr, (size_t)bytes, cudaHostRegisterPortable));
+    MI_CUDA(cudaHostRegister(h_ptr, (size_t)bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
     return MI_OK;
 }
 

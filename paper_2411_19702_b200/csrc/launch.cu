@@ -234,6 +234,32 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
                         ld_out, d_tiles, n_tiles, nullptr, (cudaStream_t)stream);
 }
 
+int mi_scatter_tiles(const void* d_src, const int32_t* d_tiles, int64_t n_tiles, int64_t n_cols, int esz, void* d_dst,
+                     int64_t ld_dst, int mirror, void* stream) {
+    if (n_cols < 1 || n_cols > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "n_cols must be in [1, 2^31)");
+    if (esz != 4 && esz != 8) return fail(MI_ERR_DOMAIN, "esz must be 4 or 8");
+    if (ld_dst < n_cols) return fail(MI_ERR_DIMENSION, "ld_dst %lld < n_cols", (long long)ld_dst);
+    if (n_tiles < 0 || n_tiles > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "bad n_tiles");
+    if (n_tiles == 0) return MI_OK;
+    if (!d_src || !d_tiles || !d_dst) return fail(MI_ERR_DOMAIN, "d_src, d_tiles and d_dst are required");
+    // pinned host destinations are written through their device alias
+    void* dst = d_dst;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, d_dst) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MI_ERR_DOMAIN, "d_dst is neither device memory nor pinned host memory");
+    }
+    if (a.type == cudaMemoryTypeHost) {
+        if (!a.devicePointer) return fail(MI_ERR_DOMAIN, "host d_dst is not mapped (register it with mi_host_register)");
+        dst = a.devicePointer;
+    } else if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+        return fail(MI_ERR_DOMAIN, "d_dst is pageable host memory: pin it (mi_host_register) first");
+    }
+    MI_CUDA(launch_scatter_tiles(d_src, d_tiles, n_tiles, mi_tile_size(), n_cols, esz, dst, ld_dst, mirror != 0,
+                                 (cudaStream_t)stream));
+    return MI_OK;
+}
+
 int mi_pack_bits(const uint8_t* d_bits, int64_t n_rows, int64_t n_cols, int64_t ld_bits, uint64_t* d_words,
                  int32_t* d_bad, void* stream) {
     int rc = check_shape(n_rows, n_cols);
@@ -323,8 +349,10 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     if (ld < mi_kmajor_ld(n_rows) || ld % 128)
         return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
                     (long long)mi_kmajor_ld(n_rows));
-    if (ld_out != MI_PACKED_UPPER && ld_out < n_cols)
-        return fail(MI_ERR_DIMENSION, "ld_out %lld < n_cols (or MI_PACKED_UPPER)", (long long)ld_out);
+    if (ld_out != MI_PACKED_UPPER && ld_out != MI_TILE_MAJOR && ld_out < n_cols)
+        return fail(MI_ERR_DIMENSION, "ld_out %lld < n_cols (or MI_PACKED_UPPER / MI_TILE_MAJOR)", (long long)ld_out);
+    if (ld_out == MI_TILE_MAJOR && row_done)
+        return fail(MI_ERR_DOMAIN, "row-band egress needs a full-matrix output");
     if (n_tiles < 0 || n_tiles > 0x7FFFFFFF) return fail(MI_ERR_DIMENSION, "bad n_tiles");
     if (n_tiles == 0) return MI_OK;
     if (out_kind == MI_OUT_COUNTS && mode != MI_MODE_EXACT)
@@ -342,7 +370,8 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     p.num_k_blocks = (int)(mi_kmajor_ld(n_rows) / 128);
     p.n_rows = (int)n_rows;
     p.m = (int)n_cols;
-    p.ld_out = ld_out;
+    p.tile_major = ld_out == MI_TILE_MAJOR ? 1 : 0;
+    p.ld_out = ld_out == MI_TILE_MAJOR ? (int64_t)mi_tile_size() : ld_out;
     p.out = d_out;
     p.eps = epsilon;
     p.include_diagonal = include_diagonal ? 1 : 0;

@@ -22,7 +22,9 @@ struct GramMiParams {
     int num_k_blocks;       // N_pad / 128
     int n_rows;             // N
     int m;                  // real columns (outputs beyond m are not written)
-    int64_t ld_out;         // output row pitch in elements
+    int64_t ld_out;         // output row pitch in elements (0: packed upper triangle)
+    int tile_major;         // 1: tile t of the list is stored at out + t TS^2 (TS x TS, row pitch TS),
+                            // no mirror (the sharded form; mi_scatter_tiles places tiles + mirrors)
     void* out;              // int32 / double / float, row-major m x ld_out
     double eps;
     int include_diagonal;
@@ -114,6 +116,12 @@ cudaError_t launch_column_order(const uint64_t* words, int64_t n_rows, int64_t m
 // out[r][c] = in[inv[r]][inv[c]] for r, c < m; esz 4 or 8 bytes
 cudaError_t launch_unpermute(const void* in, int64_t ld_in, void* out, int64_t ld_out, int64_t m, int esz,
                              const int32_t* inv, int num_sms, int smem_bytes, int ctas_per_sm, cudaStream_t stream);
+
+// Sharded-result gather (scatter.cu): tile-major shards (ts x ts per tile, tile k
+// of `tiles` at src + k ts^2) -> rows/columns of a full matrix (device or mapped
+// host memory), plus the transposed mirror of off-diagonal tiles.
+cudaError_t launch_scatter_tiles(const void* src, const int32_t* tiles, int64_t n_tiles, int ts, int64_t m, int esz,
+                                 void* dst, int64_t ld, bool mirror, cudaStream_t stream);
 
 // Tensor-peak probe (probe.cu): reps x 16 back-to-back 2-SM MMAs per SM pair;
 // d_cycles[pair] = clock64 cycles of the issuing thread.

@@ -238,7 +238,8 @@ class MIEngine:
     def _rank_mask(self, n_cols: int, rank: int, world: int) -> torch.Tensor | None:
         if world <= 1:
             return None
-        key = ("blocks", n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("shard"))
+        key = ("blocks", n_cols, rank, world, nat.get_tuning("cta_group"), nat.get_tuning("band"),
+               nat.get_tuning("shard"))
         mask = self._tiles.get(key)
         if mask is None:
             mask = torch.from_numpy(nat.rank_blocks(n_cols, rank, world)).to(self.device)
@@ -301,11 +302,13 @@ class MIEngine:
 
     def compute(self, prep: Prepared, cfg=None, out_dtype: torch.dtype = torch.float64,
                 tiles: torch.Tensor | None = None, out: torch.Tensor | None = None,
-                packed: bool = False) -> torch.Tensor:
+                packed: bool = False, tile_major: bool = False) -> torch.Tensor:
         """Kernels 2+3: fused Gram + MI over `tiles` (all upper-triangle tiles by
         default), each written with its mirror into `out` (m x m) -- or, with
         ``packed``, only j >= i into a flat m(m+1)/2 tensor (row-major upper
-        triangle; ``unpack_upper`` restores the square)."""
+        triangle; ``unpack_upper`` restores the square) -- or, with
+        ``tile_major``, tile k alone into out[k] (k x TS x TS; the sharded form
+        of dispatch.Shard)."""
         if out_dtype not in _OUT_KIND:
             raise DomainError(f"out_dtype must be float64, float32 or int32, got {out_dtype}")
         mode, eps, diag = _config_fields(cfg)
@@ -314,8 +317,21 @@ class MIEngine:
             mode = nat.MI_MODE_EXACT
         m = prep.n_cols
         if prep.perm is not None:
+            if tile_major:
+                raise DomainError("order='colsum' computes the full matrix: no tile-major output")
             return self._compute_ordered(prep, mode, eps, diag, kind, out_dtype, tiles, out, packed)
-        if packed:
+        if tile_major:
+            if tiles is None:
+                tiles = self.tiles(m)
+            ts = int(nat.lib().mi_tile_size())
+            k = int(tiles.shape[0])
+            if out is None:
+                out = torch.empty((max(k, 1), ts, ts), dtype=out_dtype, device=self.device)
+            if out.dtype != out_dtype or out.dim() != 3 or out.shape[0] < k or tuple(out.shape[1:]) != (ts, ts) \
+                    or not out.is_contiguous() or out.device != self.device:
+                raise DimensionError("tile-major out must be a contiguous (>= k, TS, TS) tensor of out_dtype")
+            ld_out = nat.MI_TILE_MAJOR
+        elif packed:
             if out is None:
                 out = torch.empty((m * (m + 1) // 2,), dtype=out_dtype, device=self.device)
             if out.dtype != out_dtype or out.dim() != 1 or out.numel() < m * (m + 1) // 2 or out.stride(0) != 1 \
@@ -416,7 +432,10 @@ class MIEngine:
                        packed: bool = False) -> torch.Tensor:
         """Host words in, host MI out, through the C ABI's mi_all_pairs_host:
         H2D, kernel 1, the fused kernel, and a D2H of finished row bands that
-        overlaps the GEMM.  ``host_out`` should be pinned for full PCIe speed.
+        overlaps the GEMM.  ``host_out``: a pinned CPU tensor / registered
+        array (D2H straight into it), or pageable memory (numpy: filled
+        through the library's pinned egress buffer by host copy threads); by
+        default a fresh numpy array.
         ``packed``: the upper triangle only (mi_all_pairs_host_packed), a flat
         m(m+1)/2 tensor -- half the device-to-host bytes."""
         mode, eps, diag = _config_fields(cfg)
@@ -434,15 +453,23 @@ class MIEngine:
                 raise DimensionError(f"words must be uint64 with shape {(n_cols, n_words(n_rows))}")
             wptr = keep.ctypes.data
         shape = (n_cols * (n_cols + 1) // 2,) if packed else (n_cols, n_cols)
+        np_dt = np.float64 if out_dtype == torch.float64 else np.float32
         if host_out is None:
-            host_out = torch.empty(shape, dtype=out_dtype, pin_memory=True)
-        if host_out.dtype != out_dtype or tuple(host_out.shape) != shape or not host_out.is_contiguous() \
-                or host_out.device.type != "cpu":
-            raise DimensionError(f"host_out must be a contiguous {shape} CPU tensor of out_dtype")
+            # ordinary (pageable) memory owned by the caller: the C ABI fills it
+            # through its cached pinned egress buffer, piece by piece
+            host_out = np.empty(shape, dtype=np_dt)
+        if isinstance(host_out, np.ndarray):
+            if host_out.dtype != np_dt or tuple(host_out.shape) != shape or not host_out.flags.c_contiguous:
+                raise DimensionError(f"host_out must be a C-contiguous {shape} {np.dtype(np_dt).name} array")
+            out_ptr = host_out.ctypes.data
+        else:
+            if host_out.dtype != out_dtype or tuple(host_out.shape) != shape or not host_out.is_contiguous() \
+                    or host_out.device.type != "cpu":
+                raise DimensionError(f"host_out must be a contiguous {shape} CPU tensor of out_dtype")
+            out_ptr = host_out.data_ptr()
         kind = nat.MI_OUT_F64 if out_dtype == torch.float64 else nat.MI_OUT_F32
         fn = nat.lib().mi_all_pairs_host_packed if packed else nat.lib().mi_all_pairs_host
-        nat.check(fn(wptr, n_rows, n_cols, mode, eps, diag, kind, host_out.data_ptr(), self.device.index),
-                  "mi_all_pairs_host")
+        nat.check(fn(wptr, n_rows, n_cols, mode, eps, diag, kind, out_ptr, self.device.index), "mi_all_pairs_host")
         del keep
         return host_out
 
@@ -460,8 +487,9 @@ def mi_all_pairs(data, cfg: EngineConfig | None = None, backend: str = "dense", 
     _config_fields(cfg)
     n, m, words = as_dense_words(data)
     eng = MIEngine.get(device)
-    host = eng.all_pairs_host(words, n, m, cfg, torch.float64)
-    return MIMatrix(values=host.numpy())
+    values = np.empty((m, m), dtype=np.float64)  # fresh, caller-owned, like the reference's
+    eng.all_pairs_host(words, n, m, cfg, torch.float64, host_out=values)
+    return MIMatrix(values=values)
 
 
 def unpack_upper(packed, m: int):

@@ -1,10 +1,11 @@
 """One host matrix that every rank on the node writes its share into.
 
 The (m, m) result lives in a POSIX shared-memory segment that rank 0 creates
-and the other ranks map; each process pins it (mi_host_register), and each
-rank copies its own tiles and mirrors into it over its own PCIe link
-(mi_copy_tiles_to_host) -- the gather does not funnel the whole matrix
-through one GPU and one link (dispatch.gather_to_root does).
+and the other ranks map; each process pins and maps it (mi_host_register),
+and each rank's GPU writes its own tiles and mirrors into it over its own
+PCIe link (dispatch.Shard.place -> mi_scatter_tiles, zero-copy) -- the gather
+does not funnel the whole matrix through one GPU and one link
+(dispatch.gather_to_root does).
 """
 
 from __future__ import annotations

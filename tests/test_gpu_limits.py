@@ -56,3 +56,26 @@ def test_operand_format_boundary(engine, n, fmt):
     assert float(np.max(np.abs(mi - ref))) < 1e-12
     del dev
     torch.cuda.empty_cache()
+
+
+def test_int8_path_multi_tile_above_2e24(engine):
+    """N = 2^24 + 77 (int8 operands, kind::i8, s32 accumulators, FP64
+    epilogue) at m = 700: three tile rows, ragged last tile, the tail split of
+    the last round.  Counts bit-exact and MI within 1e-12 against the C
+    oracle on a column subset that spans every tile boundary (MI(i, j)
+    depends only on columns i and j)."""
+    n, m = (1 << 24) + 77, 700
+    words = _words(n, m, seed=7)
+    dev = engine.upload(words)
+    g, v = engine.gram_counts(dev, n, m)
+    assert np.array_equal(v.cpu().numpy().astype(np.uint64), O.c_column_sums(words))
+    mi = engine.all_pairs_device(dev, n, m).cpu().numpy()
+    assert np.array_equal(mi, mi.T)
+    cols = np.array(sorted({0, 1, 2, 3, 4, 5, 41, 127, 128, 255, 256, 257, 383, 384, 511, 512, 513, 600, 698, 699}))
+    sub = np.ascontiguousarray(words[cols])
+    gs = g.cpu().numpy().astype(np.int64)[np.ix_(cols, cols)]
+    assert np.array_equal(gs, O.c_gram_ones(sub))
+    ref = O.c_mi_all_pairs(sub, n)
+    assert float(np.max(np.abs(mi[np.ix_(cols, cols)] - ref))) < 1e-12
+    del dev, g
+    torch.cuda.empty_cache()

@@ -29,7 +29,7 @@ def test_packed_equals_upper_triangle(engine, n, m, dtype):
     iu = np.triu_indices(m)
     assert np.array_equal(packed, full[iu])
     assert np.array_equal(unpack_upper(packed, m), full)
-    host = engine.all_pairs_host(words, n, m, None, dt, packed=True).numpy()
+    host = np.asarray(engine.all_pairs_host(words, n, m, None, dt, packed=True))
     assert np.array_equal(host, full[iu])
 
 
@@ -55,5 +55,28 @@ def test_staged_host_path_equals_device(engine, ingest, n, m):
             assert np.array_equal(host, full)
             pageable = engine.all_pairs_host(words, n, m, None, dt, host_out=torch.empty((m, m), dtype=dt)).numpy()
             assert np.array_equal(pageable, full)
+            fresh = engine.all_pairs_host(words, n, m, None, dt)  # default: a fresh numpy array
+            assert isinstance(fresh, np.ndarray) and np.array_equal(fresh, full)
     finally:
         nat.set_tuning(ingest=old)
+
+
+def test_config3_host_path_full_size(engine):
+    """The e2e path at its bench size: config 3 (N = 100,000 x m = 10,000,
+    float64) through mi_all_pairs_host -- staged upload / compute / download,
+    pageable numpy words in (host-thread staging), a fresh pageable numpy
+    output (the pinned egress buffer) -- bit-identical to the device path,
+    and through the drop-in mi_all_pairs."""
+    from paper_2411_19702_b200 import BinaryMatrix, datagen, mi_all_pairs
+
+    rec = datagen.config_recipe(3)
+    n, m = rec["n"], rec["m"]
+    dev = datagen.generate_words_device(rec, engine.device)
+    full = engine.all_pairs_device(dev, n, m).cpu().numpy()
+    words = dev.cpu().numpy().view(np.uint64)
+    host = engine.all_pairs_host(words, n, m)
+    assert isinstance(host, np.ndarray) and host.dtype == np.float64
+    assert np.array_equal(host, full)
+    res = mi_all_pairs(BinaryMatrix(n, m, words))
+    assert res.values.flags.c_contiguous and res.values.flags.owndata
+    assert np.array_equal(res.values, full)
