@@ -122,7 +122,7 @@ int mi_unpack_colsum_blocks(const uint64_t* d_words, int64_t n_rows, int64_t n_c
 /* mi_unpack_colsum_blocks in pieces, for staged ingest (words arriving by
  * column groups): mi_unpack_prep once (per-column counters, block ranges, the
  * fixed-point table), then mi_unpack_colsum_range for columns [c_begin, c_end)
- * (c_begin a multiple of 32, c_end <= mi_kmajor_rows(n_cols)) once their
+ * (c_begin and c_end multiples of 32, c_end <= mi_kmajor_rows(n_cols)) once their
  * words are on the device; the ranges must cover every column before the
  * tiles that need them run. */
 int mi_unpack_prep(int64_t n_rows, int64_t n_cols, void* d_colstat, void* stream);

@@ -214,8 +214,12 @@ int mi_unpack_colsum_range(const uint64_t* d_words, int64_t n_rows, int64_t n_co
                     (long long)mi_kmajor_ld(n_rows));
     if (!d_colstat) return fail(MI_ERR_DOMAIN, "d_colstat is required");
     const int64_t m_pad = mi_kmajor_rows(n_cols);
-    if (c_begin < 0 || c_begin % 32 || c_end > m_pad || c_begin >= c_end)
-        return fail(MI_ERR_DIMENSION, "column range [%lld, %lld) must start at a multiple of 32 and lie in [0, %lld)",
+    // both ends on multiples of 32: colstat_kernel's per-warp min/max reductions
+    // need every lane of the range's last warp (m_pad is a multiple of 256, so
+    // the last range can always end there)
+    if (c_begin < 0 || c_begin % 32 || c_end % 32 || c_end > m_pad || c_begin >= c_end)
+        return fail(MI_ERR_DIMENSION,
+                    "column range [%lld, %lld) must start and end on multiples of 32 and lie in [0, %lld]",
                     (long long)c_begin, (long long)c_end, (long long)m_pad);
     DevInfo info;
     if ((rc = current_device_info(&info))) return rc;

@@ -227,7 +227,7 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
                                 int64_t m_pad, int32_t* colsum, ColStat* colstat, int2* blkrange, bool fp4,
                                 const uint8_t* block_mask, int tile, int64_t c_begin, int64_t c_end, int num_sms,
                                 cudaStream_t stream, const int32_t* perm) {
-    if (c_begin % kUnpackCols || c_end > m_pad || c_begin >= c_end) return cudaErrorInvalidValue;
+    if (c_begin % kUnpackCols || c_end % kUnpackCols || c_end > m_pad || c_begin >= c_end) return cudaErrorInvalidValue;
     const int fix_s = xlogx_scale(n_rows);
     {
         // tools/unpack_bench.py sweeps (r01h, r01m): 32 k-blocks per block and 16

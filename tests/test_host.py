@@ -126,6 +126,11 @@ def test_c_abi_rejects_bad_arguments_without_device_work():
     assert rc == nat.MI_ERR_DIMENSION
     with pytest.raises(DomainError):
         nat.check(nat.MI_ERR_DOMAIN, "x")
+    # column ranges must start and end on multiples of 32 (colstat_kernel's warp reductions)
+    ld = int(lib.mi_kmajor_ld(1000))
+    for c0, c1 in ((0, 40), (16, 64), (64, 32), (0, 544)):
+        rc = lib.mi_unpack_colsum_range(None, 1000, 300, None, ld, 1, None, None, c0, c1, None)
+        assert rc == nat.MI_ERR_DIMENSION and "multiples of 32" in nat.last_error(), (c0, c1)
     words = np.array([[0b111]], dtype=np.uint64)  # dirty padding for n_rows = 2
     out = np.empty((1, 1))
     rc = lib.mi_all_pairs_host(words.ctypes.data, 2, 1, 0, 1e-12, 1, 1, out.ctypes.data, 0)
