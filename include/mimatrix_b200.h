@@ -136,6 +136,23 @@ int mi_unpack_colsum_range(const uint64_t* d_words, int64_t n_rows, int64_t n_co
 int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols,
                int64_t ld, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
                int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
+/* ---- word-operand path (tall-N / narrow-m) ----
+ * The same fused Gram + MI, reading the packed words themselves (the
+ * reference's gram_ones_kernel reads them too, _kernels.py:36-45): producer
+ * warps expand each k-block of 256 rows into the swizzled shared-memory
+ * stages, so the e2m1 operand X never exists in HBM (for narrow m its write
+ * and read-back cost more than the MMAs).  d_colstat comes from
+ * mi_colstat_words (column sums and statistics only: one read of the words,
+ * no expansion).  Needs e2m1 operands (n_rows < 2^24, SM-pair tiles).
+ * Same outputs, tile lists and ld_out forms as mi_gram_mi; bit-identical. */
+/* 1 when the engine's rule ("xp" / "xp_cols" knobs) picks the word-operand
+ * path for this shape, else 0 (the unpack + TMA path). */
+int mi_words_operand(int64_t n_rows, int64_t n_cols);
+int mi_colstat_words(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, void* d_colstat, int32_t* d_colsum,
+                     void* stream);
+int mi_gram_mi_words(const uint64_t* d_words, const void* d_colstat, int64_t n_rows, int64_t n_cols, int mode,
+                     double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
+                     const int32_t* d_tiles, int64_t n_tiles, void* stream);
 /* binmat.from_bits / from_rows (binmat.py:34-46,136-172) on the device: a
  * row-major uint8 0/1 matrix (n_rows x n_cols, row pitch ld_bits bytes) ->
  * the words layout (n_cols x ceil(n_rows/64) uint64, padding bits zero).
@@ -244,8 +261,10 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * "ingest_split" (0 = even group sizes, default; 1 = doubling), "serp" (1 =
  * odd tile rounds sweep K backwards for L2 reuse across rounds; 0 default),
  * "f32_epi" (float32 output, exact mode: tiles off the table path run the
- * FP32-pipe epilogue beside the next tile's MMAs; 1 default, 0 = FP64).  Also
- * settable as MI_B200_<KEY> env vars. */
+ * FP32-pipe epilogue beside the next tile's MMAs; 1 default, 0 = FP64), "xp"
+ * (the word-operand build of mi_all_pairs_host and the Python engine: -1 auto
+ * = when m_pad <= "xp_cols", default 2048; 0 never; 1 whenever the operands
+ * are e2m1).  Also settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */
 /* release the cached device workspaces of mi_*_host */

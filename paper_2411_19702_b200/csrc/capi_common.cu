@@ -63,7 +63,8 @@ Tuning& tuning() {
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
-                       env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1)};
+                       env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1), env_int("MI_B200_XP", -1),
+                       env_int("MI_B200_XP_COLS", 2048)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -72,6 +73,16 @@ int cta_group() { return tuning().cta_group; }
 // int8.  mi_unpack_colsum and mi_gram_mi both follow this rule, so the knob
 // must not change between them.
 bool operand_fp4(int64_t n_rows) { return tuning().fp4 && tuning().cta_group == 2 && n_rows < kFp4MaxN; }
+// The word-operand build (expansion inside the GEMM's producer, no X in HBM)
+// where writing and re-reading X costs a large share of the step: narrow m
+// (the unpack is O(N m), the GEMM O(N m^2)).  Knob "xp": -1 auto (m_pad <=
+// "xp_cols"), 0 never, 1 whenever the operands are e2m1.
+bool words_operand(int64_t n_rows, int64_t n_cols) {
+    const Tuning& t = tuning();
+    // (the words' TMA map needs a row pitch of a multiple of 16 bytes: nw even)
+    if (!operand_fp4(n_rows) || t.xp == 0 || ((n_rows + 63) / 64) % 2 != 0) return false;
+    return t.xp == 1 || round_up(n_cols < 1 ? 1 : n_cols, 256) <= t.xp_cols;
+}
 int prefetch_dist() { return tuning().prefetch; }
 int l2_hint() { return tuning().l2_hint; }
 int tile_band() { return tuning().band > 0 ? tuning().band : 8; }
@@ -196,6 +207,8 @@ int64_t mi_colstat_bytes(int64_t n_rows, int64_t n_cols) {
 
 int mi_tile_size(void) { return gram_mi_tile_size(cta_group()); }
 
+int mi_words_operand(int64_t n_rows, int64_t n_cols) { return words_operand(n_rows, n_cols) ? 1 : 0; }
+
 int mi_set_tuning(const char* key, int value) {
     if (!key) return fail(MI_ERR_DOMAIN, "null tuning key");
     Tuning& t = tuning();
@@ -253,6 +266,14 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "f32_epi")) {
         if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "f32_epi must be 0 (FP64) or 1 (FP32 pipe)");
         t.f32_epi = value;
+    } else if (!strcmp(key, "debug")) {  // experiments only (GramMiParams::debug bit mask)
+        t.debug = value;
+    } else if (!strcmp(key, "xp")) {
+        if (value < -1 || value > 1) return fail(MI_ERR_DOMAIN, "xp must be -1 (auto), 0 (off) or 1 (on)");
+        t.xp = value;
+    } else if (!strcmp(key, "xp_cols")) {
+        if (value < 0) return fail(MI_ERR_DOMAIN, "xp_cols must be >= 0");
+        t.xp_cols = value;
     } else if (!strcmp(key, "epi_warps")) {
         if (value != 8 && value != 16) return fail(MI_ERR_DOMAIN, "epi_warps must be 8 or 16");
         t.epi_warps = value;
@@ -284,6 +305,9 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "ingest_split")) return t.ingest_split;
     if (!strcmp(key, "serp")) return t.serp;
     if (!strcmp(key, "f32_epi")) return t.f32_epi;
+    if (!strcmp(key, "xp")) return t.xp;
+    if (!strcmp(key, "debug")) return t.debug;
+    if (!strcmp(key, "xp_cols")) return t.xp_cols;
     return -1;
 }
 

@@ -73,6 +73,28 @@ cudaError_t launch_gram_mi(int cg, bool fp4, int out_kind, int mode, int stages,
     return cudaErrorInvalidValue;
 }
 
+#define MI_XP_EXTERN(OV, MV) \
+    extern template cudaError_t launch_impl<2, OV, MV, kXpStages, kXpEpiWarps, false, true, true>(const CUtensorMap&, const GramMiParams&, int, cudaStream_t);
+MI_XP_EXTERN(MI_OUT_F64, MI_MODE_EXACT)
+MI_XP_EXTERN(MI_OUT_F64, MI_MODE_EPSILON)
+MI_XP_EXTERN(MI_OUT_F32, MI_MODE_EXACT)
+MI_XP_EXTERN(MI_OUT_F32, MI_MODE_EPSILON)
+MI_XP_EXTERN(MI_OUT_COUNTS, MI_MODE_EXACT)
+#undef MI_XP_EXTERN
+
+cudaError_t launch_gram_mi_words(int out_kind, int mode, const CUtensorMap& tmap, const GramMiParams& p, int num_sms,
+                                 cudaStream_t stream) {
+#define MI_XP_DISPATCH(OV, MV) \
+    if (out_kind == OV && mode == MV) return launch_impl<2, OV, MV, kXpStages, kXpEpiWarps, false, true, true>(tmap, p, num_sms, stream);
+    MI_XP_DISPATCH(MI_OUT_F64, MI_MODE_EXACT)
+    MI_XP_DISPATCH(MI_OUT_F64, MI_MODE_EPSILON)
+    MI_XP_DISPATCH(MI_OUT_F32, MI_MODE_EXACT)
+    MI_XP_DISPATCH(MI_OUT_F32, MI_MODE_EPSILON)
+    MI_XP_DISPATCH(MI_OUT_COUNTS, MI_MODE_EXACT)
+#undef MI_XP_DISPATCH
+    return cudaErrorInvalidValue;
+}
+
 int gram_mi_tile_size(int cg) { return 128 * cg; }
 
 }  // namespace mib200

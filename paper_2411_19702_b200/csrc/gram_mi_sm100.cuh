@@ -71,17 +71,29 @@ struct ColS {
 };
 constexpr uint32_t kTabBytes = 128u * 16u;  // log2_frac double2 table
 
-template <int CG, int ST>
+// XP builds: a ring of raw-word stages in front of the operand ring.  One raw
+// stage holds, per operand half, 128 columns x 128 bytes of packed words (16
+// words = 4 k-blocks of 256 rows each: every column row is one full 128-byte
+// line of the words array), loaded by TMA with the 128-byte swizzle.
+constexpr int kXpRawStages = 2;
+constexpr int kXpKbPerRaw = 4;                 // k-blocks per raw stage
+constexpr int kXpPrefetch = 6;                 // raw stages of L2 prefetch ahead of the TMA loads
+constexpr uint32_t kXpRawHalfBytes = 128 * 128;
+
+template <int CG, int ST, bool XP = false>
 struct SmemLayout {
     static constexpr uint32_t CSZ = (uint32_t)sizeof(ColS);
     static constexpr uint32_t TABB = kTabBytes;
+    static constexpr int RS = XP ? kXpRawStages : 0;
     static constexpr uint32_t a_off = 0;
     static constexpr uint32_t b_off = ST * kStageHalfBytes;
-    static constexpr uint32_t tab_off = 2 * ST * kStageHalfBytes;  // log tables
+    static constexpr uint32_t raw_off = 2 * ST * kStageHalfBytes;   // XP: raw stages [RS][A, B]
+    static constexpr uint32_t tab_off = raw_off + RS * 2 * kXpRawHalfBytes;  // log tables
     static constexpr uint32_t col_off = tab_off + TABB;            // column stats [2][TS]
     static constexpr uint32_t bar_off = col_off + 2 * 128 * CG * CSZ;
-    // full[ST], empty[ST], tfull[2], tempty[2], tmem slot, pacing words
-    static constexpr uint32_t pace_off = bar_off + (2 * ST + 4) * 8 + 8;
+    // full[ST], empty[ST], tfull[2], tempty[2], tmem slot, (XP) raw_full[RS], raw_empty[RS], pacing words
+    static constexpr uint32_t raw_bar_off = bar_off + (2 * ST + 4) * 8 + 8;
+    static constexpr uint32_t pace_off = raw_bar_off + 2 * RS * 8;
     static constexpr uint32_t bytes = pace_off + 16;
     // + alignment slack when it fits (the dynamic window is normally 1 KB aligned)
     static constexpr uint32_t request = bytes + 1024 <= kMaxSmem ? bytes + 1024 : kMaxSmem;
@@ -494,12 +506,41 @@ __device__ __noinline__ void mma_tail(uint32_t tmem_base, int width, int kb0, in
     umma_commit<CG>(bar0 + 8u * (2 * ST + acc));  // tfull[acc]
 }
 
-template <int CG, int OUT, int MODE, int ST, int EW, bool PACE, bool FP4>
-__global__ void __launch_bounds__(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1)
+// Threads of a build: producer + MMA + epilogue warps, the pacer slot (PACE
+// builds; XP builds keep the slot idle), and the XP builds' expander warps.
+template <int CG, int EW, bool PACE, bool XP>
+constexpr int kernel_threads() {
+    return Cfg<CG, EW>::THREADS + ((PACE || XP) ? 32 : 0) + (XP ? 32 * kXpWarps : 0);
+}
+
+// XP: one step of a word-operand producer -- 32 bytes of packed words (256
+// rows of one column, one k-block) -> the column's 128-byte row of the
+// stage, e2m1 nibbles 0 / 1.0 (0b0010).  Bit b of 32-bit word c (rows 32c ..
+// 32c + 31 of the k-block) goes to nibble 8 (b & 3) + (b >> 2) of 16-byte
+// chunk c; any bijection rows -> K slots serves, as long as every column uses
+// the same one (both operands are rows of X), and this one costs one shift
+// and one AND per 8 nibbles.  Chunk c lands at 16-byte slot c ^ (row & 7):
+// the 128-byte swizzle the UMMA descriptors (and TMA) use.  A warp's 32
+// consecutive rows fill each 128-byte bank line once per store: no conflicts.
+__device__ __forceinline__ void xp_put_row(uint32_t row_addr, uint32_t sw, const uint64_t (&w)[4]) {
+    constexpr uint32_t M = 0x22222222u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t x = h ? (uint32_t)(w[q] >> 32) : (uint32_t)w[q];
+            const uint32_t c = (uint32_t)(2 * q + h);
+            sts128(row_addr + ((c ^ sw) << 4), (x << 1) & M, x & M, (x >> 1) & M, (x >> 2) & M);
+        }
+    }
+}
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE, bool FP4, bool XP = false>
+__global__ void __launch_bounds__(kernel_threads<CG, EW, PACE, XP>(), 1)
 gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p) {
+    static_assert(!XP || (FP4 && CG == 2 && !PACE), "word-operand builds: e2m1 on CTA pairs, unpaced");
     using C = Cfg<CG, EW>;
     using T = typename OutT<OUT>::T;
-    using L = SmemLayout<CG, ST>;
+    using L = SmemLayout<CG, ST, XP>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     const uint32_t base = (raw_addr + 1023u) & ~1023u;  // SW128 needs 1024-B alignment
@@ -531,12 +572,17 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_x);
         for (int s = 0; s < ST; ++s) {
-            mbar_init(full_bar(s), 1);
+            // XP: every expander warp of both CTAs arrives on the leader's full barrier
+            mbar_init(full_bar(s), XP ? CG * kXpRowWarps : 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
             mbar_init(tempty_bar(a), CG * EW);
+        }
+        for (int r = 0; r < L::RS; ++r) {  // XP raw ring: TMA bytes in, expander warps out
+            mbar_init(base + L::raw_bar_off + 8u * r, 1);
+            mbar_init(base + L::raw_bar_off + 8u * (L::RS + r), kXpWarps);
         }
         fence_mbarrier_init();
         s_pace[0] = 0u;
@@ -584,8 +630,29 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     // them once from HBM instead of once per pair (tall N overflows the L2).
     // (a separate instantiation: the check costs ~5% in the producer loop of short-K shapes)
     const bool pacing = PACE && p.pace != nullptr && p.pace_window > 0 && rank == 0 && n_clusters <= kPaceMaxClusters;
+    // XP: this cluster's work as segments -- its main tiles (full K), then its
+    // tail unit -- walked identically by the raw producer, the expanders and
+    // the MMA warp
+    const int n_main = cluster < p.n_full ? (p.n_full - 1 - cluster) / n_clusters + 1 : 0;
+    const int n_seg = n_main + (has_tail ? 1 : 0);
+    // segment sg: operand half rows (first column of A's and B's half), K range, B = A
+    auto seg = [&](int sg, int& ra0, int& rb0, int& kb0, int& kb1, bool& share) {
+        const int2 tl = p.tiles[sg < n_main ? cluster + sg * n_clusters : tail_t];
+        ra0 = tl.x * C::TS + (int)rank * 128;
+        if (sg < n_main) {
+            rb0 = tl.y * C::TS + (int)rank * 128;
+            kb0 = 0;
+            kb1 = nkb;
+            share = tl.x == tl.y;
+        } else {
+            rb0 = tl.y * C::TS + (tail_k ? 0 : tail_c * tail_w) + (int)rank * (tail_w / CG);
+            kb0 = tail_kb0;
+            kb1 = tail_kb1;
+            share = tl.x == tl.y && tail_w == C::TS;
+        }
+    };
 
-    if (warp == 0) {
+    if (warp == 0 && !XP) {
         // ================= TMA producer =================
         // The whole warp runs the loop (warp-uniform control flow: descriptors
         // and coordinates stay in uniform registers) and one elected lane
@@ -682,6 +749,49 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             mbar_wait(empty_bar(s), ph ^ 1u);
             if (++s == ST) { s = 0; ph ^= 1u; }
         }
+    } else if (XP && warp == 1) {
+        // ================= MMA issuer (XP) =================
+        // One warp-uniform loop over the segments (main tiles and the tail
+        // unit alike; descriptors stay in uniform registers), one elected lane
+        // issues.  Diagonal tiles read B from the A stage.
+        if constexpr (XP) {
+            if (rank == 0) {
+                const uint64_t adesc0 = umma_desc_sw128_kmajor(sA);
+                const uint64_t bdesc0 = umma_desc_sw128_kmajor(sB);
+                int s = 0, acc = 0;
+                uint32_t ph = 0, aph = 0;
+                for (int sg = 0; sg < n_seg; ++sg) {
+                    int ra0, rb0, kb0, kb1;
+                    bool share;
+                    seg(sg, ra0, rb0, kb0, kb1, share);
+                    // tail column slices: an M x W accumulator in TMEM columns [0, W)
+                    const uint32_t idesc = mma_idesc<CG, FP4>(C::MMA_M, sg < n_main ? C::MMA_N : tail_w);
+                    const uint64_t bd = share ? adesc0 : bdesc0;
+                    mbar_wait(tempty_bar(acc), aph ^ 1u);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(full_bar(s), ph);
+                        tc_fence_after();
+                        const uint64_t soff = (uint64_t)(s * (kStageHalfBytes >> 4));
+                        if (elect_one()) {
+                            if (!(p.debug & 16)) {
+#pragma unroll
+                                for (int k = 0; k < kBK / 32; ++k)
+                                    mma_step<CG, FP4>(d_tmem, adesc0 + soff + 2u * k, bd + soff + 2u * k, idesc,
+                                                      tmem_base, (kb != kb0 || k != 0) ? 1u : 0u);
+                            }
+                            umma_commit<CG>(empty_bar(s));
+                        }
+                        __syncwarp();
+                        if (++s == ST) { s = 0; ph ^= 1u; }
+                    }
+                    if (elect_one()) umma_commit<CG>(tfull_bar(acc));
+                    __syncwarp();
+                    if (++acc == NACC) { acc = 0; aph ^= 1u; }
+                }
+            }
+        }
     } else if (warp == 1) {
         // ================= MMA issuer =================
         // (warp-uniform loop, one elected lane issues; see the producer)
@@ -738,6 +848,170 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             }
             if (has_tail && lane == 0)
                 mma_tail<CG, ST, FP4>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
+        }
+    } else if (XP && (warp == 0 || warp >= C::PACER_WARP)) {
+        // ================= word operands (XP) =================
+        // warp 0 (one lane): TMA of raw packed words -- per operand half, 128
+        //   columns x 16 words (4 k-blocks) -- into the raw ring (this CTA's
+        //   barriers; each CTA loads its own halves);
+        // warps PACER_WARP + 1 .. + kXpWarps (expanders): thread xt owns row xt
+        //   of the CTA's halves of A and B; per k-block it reads its 32 bytes
+        //   of words from the raw stage, writes the swizzled e2m1 rows
+        //   (xp_put_row), fences them into the async proxy and arrives (one
+        //   lane per warp) on the leader CTA's full barrier.  The expanders
+        //   have no global loads in flight at that fence (TMA brings the
+        //   words), so it costs a shared-memory drain, not a DRAM latency.
+        // The pacer slot idles.  Diagonal tiles stage one copy (B = A).
+        if constexpr (XP) {
+            const bool spin = (p.debug & 256) != 0;  // experiments: spin instead of suspend-hinted waits
+            auto xwait = [&](uint32_t bar, uint32_t par) {
+                if (spin) mbar_wait_spin(bar, par);
+                else mbar_wait(bar, par);
+            };
+            // experiments: per-phase cycle sums of cluster 0 (tools/xp_probe.py --trace)
+            long long* const xtr = (p.trace && cluster == 0) ? p.trace + 2048 : nullptr;
+            const uint32_t raw0 = base + L::raw_off;
+            const uint32_t rbar0 = base + L::raw_bar_off;
+            auto raw_full = [&](int r) { return rbar0 + 8u * r; };
+            auto raw_empty = [&](int r) { return rbar0 + 8u * (L::RS + r); };
+            auto raw_a = [&](int r) { return raw0 + (uint32_t)r * 2u * kXpRawHalfBytes; };
+            if (warp == 0) {
+                const uint64_t policy = p.l2_hint == 1   ? l2_policy_evict_last()
+                                        : p.l2_hint == 2 ? l2_policy_evict_first()
+                                                         : l2_policy_evict_normal();
+                int r = 0;
+                uint32_t rph = 0;
+                long long pw = 0;
+                for (int sg = 0; sg < n_seg; ++sg) {
+                    int ra0, rb0, kb0, kb1;
+                    bool share;
+                    seg(sg, ra0, rb0, kb0, kb1, share);
+                    const int qlast = (kb1 - 1) / kXpKbPerRaw;
+                    // L2 prefetch of the raw boxes kXpPrefetch stages ahead: the raw ring
+                    // holds only kXpRawStages x 4 k-blocks, less than a DRAM round trip
+                    for (int q = kb0 / kXpKbPerRaw; q < min(qlast + 1, kb0 / kXpKbPerRaw + kXpPrefetch); ++q)
+                        if (elect_one()) {
+                            tma_prefetch_2d(&tmap_x, 4 * kXpKbPerRaw * q, ra0);
+                            if (!share) tma_prefetch_2d(&tmap_x, 4 * kXpKbPerRaw * q, rb0);
+                        }
+                    for (int q = kb0 / kXpKbPerRaw; q <= qlast; ++q) {
+                        if (q + kXpPrefetch <= qlast && elect_one()) {
+                            tma_prefetch_2d(&tmap_x, 4 * kXpKbPerRaw * (q + kXpPrefetch), ra0);
+                            if (!share) tma_prefetch_2d(&tmap_x, 4 * kXpKbPerRaw * (q + kXpPrefetch), rb0);
+                        }
+                        __syncwarp();
+                        const long long c0 = xtr ? clock64() : 0;
+                        xwait(raw_empty(r), rph ^ 1u);
+                        if (xtr) pw += clock64() - c0;
+                        if (p.debug & 64) {  // experiments: no word loads (expander throughput alone)
+                            if (elect_one()) mbar_arrive_local(raw_full(r));
+                        } else if (elect_one()) {
+                            mbar_arrive_expect_tx(raw_full(r), (share ? 1u : 2u) * kXpRawHalfBytes);
+                            tma_load_2d_local(raw_a(r), &tmap_x, raw_full(r), 4 * kXpKbPerRaw * q, ra0, policy);
+                            if (!share)
+                                tma_load_2d_local(raw_a(r) + kXpRawHalfBytes, &tmap_x, raw_full(r),
+                                                  4 * kXpKbPerRaw * q, rb0, policy);
+                        }
+                        __syncwarp();
+                        if (++r == L::RS) { r = 0; rph ^= 1u; }
+                    }
+                }
+                if (xtr && lane == 0) xtr[24 + rank] = pw;
+            } else if (warp > C::PACER_WARP) {
+                // Two groups of kXpRowWarps warps: within each raw stage (4
+                // k-blocks), group 0 expands the first two k-blocks and group 1
+                // the last two, so two batches are in flight per row and every
+                // scheduler runs two expander warps.  Operand stage of a k-block
+                // = its position in this CTA's k-block sequence modulo ST.
+                const int xw = warp - C::PACER_WARP - 1;
+                const int grp = xw / kXpRowWarps;
+                const int xt = (xw % kXpRowWarps) * 32 + (int)lane;
+                const uint32_t full_leader0 = map_to_cta(full_bar(0), 0u);
+                const uint32_t sw = (uint32_t)xt & 7u;
+                int r = 0;
+                uint32_t rph = 0;
+                long long ctr = 0;  // k-blocks of this CTA's sequence before the current raw stage
+                long long acc_t[6] = {0, 0, 0, 0, 0, 0};  // experiments (xtr): phase cycle sums
+                for (int sg = 0; sg < n_seg; ++sg) {
+                    int ra0, rb0, kb0, kb1;
+                    bool share;
+                    seg(sg, ra0, rb0, kb0, kb1, share);
+                    for (int q = kb0 / kXpKbPerRaw; q <= (kb1 - 1) / kXpKbPerRaw; ++q) {
+                        const int lo = max(kb0, q * kXpKbPerRaw), hi = min(kb1, (q + 1) * kXpKbPerRaw);
+                        const int my0 = max(lo, q * kXpKbPerRaw + 2 * grp), my1 = min(hi, q * kXpKbPerRaw + 2 * grp + 2);
+                        const long long c0 = xtr ? clock64() : 0;
+                        xwait(raw_full(r), rph);
+                        if (xtr) acc_t[0] += clock64() - c0;
+                        if (my1 > my0) {
+                            const bool two = my1 - my0 == 2;
+                            const long long cA = ctr + (my0 - lo);
+                            const int s0 = (int)(cA % ST), s1 = (int)((cA + 1) % ST);
+                            const uint32_t p0 = (uint32_t)((cA / ST) & 1), p1 = (uint32_t)(((cA + 1) / ST) & 1);
+                            const long long t0 = xtr ? clock64() : 0;
+                            // k-block j's 32 bytes: logical chunks 2j, 2j + 1 of the swizzled 128-byte row
+                            const uint32_t j = (uint32_t)(my0 - q * kXpKbPerRaw);
+                            const uint32_t rowa = raw_a(r) + (uint32_t)xt * 128u;
+                            uint64_t wa[2][4], wb[2][4];
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) {
+                                if (i == 0 || two) {
+                                    const uint32_t jj = j + (uint32_t)i;
+                                    lds128(rowa + (((2u * jj) ^ sw) << 4), wa[i][0], wa[i][1]);
+                                    lds128(rowa + (((2u * jj + 1u) ^ sw) << 4), wa[i][2], wa[i][3]);
+                                    if (!share) {
+                                        lds128(rowa + kXpRawHalfBytes + (((2u * jj) ^ sw) << 4), wb[i][0], wb[i][1]);
+                                        lds128(rowa + kXpRawHalfBytes + (((2u * jj + 1u) ^ sw) << 4), wb[i][2], wb[i][3]);
+                                    }
+                                }
+                            }
+                            const long long t1 = xtr ? clock64() : 0;
+                            xwait(empty_bar(s0), p0 ^ 1u);
+                            if (two) xwait(empty_bar(s1), p1 ^ 1u);
+                            const long long t2 = xtr ? clock64() : 0;
+                            if (!(p.debug & 32)) {  // experiments: 32 = no expansion (load pipeline alone)
+#pragma unroll
+                                for (int i = 0; i < 2; ++i) {
+                                    if (i == 0 || two) {
+                                        const uint32_t so = (uint32_t)(i ? s1 : s0) * kStageHalfBytes + (uint32_t)xt * 128u;
+                                        xp_put_row(sA + so, sw, wa[i]);
+                                        if (!share) xp_put_row(sB + so, sw, wb[i]);
+                                    }
+                                }
+                            }
+                            const long long t3 = xtr ? clock64() : 0;
+                            // Publish: the proxy fence drains this thread's shared-memory writes
+                            // (MEMBAR.CTA) and makes them visible to the async proxy; the arrives
+                            // that follow are relaxed.  A release.cluster arrive would add a
+                            // GPU-wide drain per warp and batch (~800 cycles measured; the
+                            // pipeline is latency-bound: tools/xp_probe.py), and the data are
+                            // already in this SM's shared memory when the arrive lands.
+                            fence_proxy_async_smem();
+                            __syncwarp();
+                            if (lane == 0) {
+                                mbar_arrive_cluster_relaxed(full_leader0 + 8u * s0);
+                                if (two) mbar_arrive_cluster_relaxed(full_leader0 + 8u * s1);
+                            }
+                            if (xtr) {
+                                acc_t[1] += t1 - t0;           // LDS
+                                acc_t[2] += t2 - t1;           // waiting for free stages
+                                acc_t[3] += t3 - t2;           // expand + STS
+                                acc_t[4] += clock64() - t3;    // fence + arrive
+                                acc_t[5] += two ? 2 : 1;       // k-blocks
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_local(raw_empty(r));  // both groups are done with it
+                        if (++r == L::RS) { r = 0; rph ^= 1u; }
+                        ctr += hi - lo;
+                    }
+                }
+                if (xtr && xw == 0 && lane == 0)
+                    for (int k = 0; k < 6; ++k) xtr[8 * rank + k] = acc_t[k];
+                // drain: the last commit of every stage must land before exit
+                if (xw == 0) {
+                    for (int q = 0; q < ST; ++q, ++ctr) xwait(empty_bar((int)(ctr % ST)), (uint32_t)(((ctr / ST) & 1) ^ 1));
+                }
+            }
         }
     } else if (PACE && warp == C::PACER_WARP) {
         // ================= pacer =================
@@ -833,11 +1107,11 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 use_f32 = OUT == MI_OUT_F32 && MODE == MI_MODE_EXACT && p.f32_epi && !use_table;
                 use_hybrid = have_table && !use_table && !use_f32 && p.hybrid;
                 if (use_f32) {
-                    if (etid < C::TS) colsf[etid] = p.colstat[tile.y * C::TS + etid].f;
+                    for (int e = etid; e < C::TS; e += EW * 32) colsf[e] = p.colstat[tile.y * C::TS + e].f;
                     named_barrier_sync(2, EW * 32);
                     Af = p.colstat[i].f;
                 } else {
-                    if (etid < C::TS) cols[etid] = col_s(p.colstat[tile.y * C::TS + etid]);
+                    for (int e = etid; e < C::TS; e += EW * 32) cols[e] = col_s(p.colstat[tile.y * C::TS + e]);
                     named_barrier_sync(2, EW * 32);
                     Arow = col_s(p.colstat[i]);  // colstat has m_pad entries
                     AQ = RowQ{Arow.vi, p.n_rows - Arow.vi, nln - Arow.q};
@@ -1032,10 +1306,10 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
 
 // ---------------------------------------------------------------- launch
 
-template <int CG, int OUT, int MODE, int ST, int EW, bool PACE, bool FP4>
+template <int CG, int OUT, int MODE, int ST, int EW, bool PACE, bool FP4, bool XP = false>
 cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream) {
-    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW, PACE, FP4>;
-    constexpr uint32_t smem = SmemLayout<CG, ST>::request;
+    auto kern = gram_mi_kernel<CG, OUT, MODE, ST, EW, PACE, FP4, XP>;
+    constexpr uint32_t smem = SmemLayout<CG, ST, XP>::request;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int max_clusters = num_sms / CG;
@@ -1048,7 +1322,7 @@ cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG, 1, 1);
-    cfg.blockDim = dim3(Cfg<CG, EW>::THREADS + (PACE ? 32 : 0), 1, 1);
+    cfg.blockDim = dim3(kernel_threads<CG, EW, PACE, XP>(), 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];

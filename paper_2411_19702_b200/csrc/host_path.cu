@@ -231,12 +231,14 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     const int64_t ld = mi_kmajor_ld(n_rows);
     const int64_t m_pad = mi_kmajor_rows(n_cols);
     int rc;
+    // the word-operand build needs no X: kernel 1 only counts (x = nullptr)
+    const bool xp = words_operand(n_rows, n_cols);
     if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
-    if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if (!xp && (rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
     if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
     if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
     if ((rc = upload_words(ws, h_words, n_cols, nw))) return rc;
-    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
+    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, xp ? nullptr : (int8_t*)ws.x, ld, m_pad,
                                  (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
                                  blkrange_ptr(ws.colstat, n_rows, n_cols), fixr_ptr(ws.colstat, n_rows, n_cols),
                                  operand_fp4(n_rows), nullptr,
@@ -270,8 +272,10 @@ int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t
     if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
     MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
     (void)info;
-    return launch_fused((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps, include_diagonal, out_kind,
-                        d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, row_done, ws.stream);
+    const bool xp = words_operand(n_rows, n_cols);
+    return launch_fused(xp ? nullptr : (const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps, include_diagonal,
+                        out_kind, d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, row_done, ws.stream,
+                        xp ? (const uint64_t*)ws.words : nullptr);
 }
 
 }  // namespace capi
@@ -325,8 +329,9 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
     if (blk.back() != T) blk.push_back(T);
     S = (int)blk.size() - 1;
     int rc;
+    const bool xp = words_operand(n_rows, n_cols);  // no X: the GEMM expands the words itself
     if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
-    if ((rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if (!xp && (rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
     if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
     if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
     if ((rc = ensure(&ws.out, &ws.out_cap, (size_t)n_cols * (size_t)n_cols * esz))) return rc;
@@ -415,12 +420,12 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
                                 cudaMemcpyHostToDevice, ws.stream));
         mark(ws.stream);  // H2D g done
         const int64_t u1 = g == S - 1 ? m_pad : blk[g + 1] * tile;
-        MI_CUDA(launch_unpack_range((const uint64_t*)ws.words, n_rows, n_cols, nw, (int8_t*)ws.x, ld, m_pad,
-                                    (int32_t*)ws.colsum, cs, xl ? br : nullptr, fp4, nullptr, tile, blk[g] * tile, u1,
-                                    info.num_sms, ws.stream));
-        if ((rc = launch_fused((const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, epsilon, include_diagonal,
-                               out_kind, ws.out, n_cols, (const int32_t*)ws.tiles + 2 * first[g],
-                               first[g + 1] - first[g], nullptr, ws.stream)))
+        MI_CUDA(launch_unpack_range((const uint64_t*)ws.words, n_rows, n_cols, nw, xp ? nullptr : (int8_t*)ws.x, ld,
+                                    m_pad, (int32_t*)ws.colsum, cs, xl ? br : nullptr, fp4, nullptr, tile,
+                                    blk[g] * tile, u1, info.num_sms, ws.stream));
+        if ((rc = launch_fused(xp ? nullptr : (const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, epsilon,
+                               include_diagonal, out_kind, ws.out, n_cols, (const int32_t*)ws.tiles + 2 * first[g],
+                               first[g + 1] - first[g], nullptr, ws.stream, xp ? (const uint64_t*)ws.words : nullptr)))
             return rc;
         MI_CUDA(cudaEventRecord(ws.stage_ev[g], ws.stream));
         mark(ws.stream);  // compute g done

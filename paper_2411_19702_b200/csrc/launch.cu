@@ -154,6 +154,24 @@ int make_tmap(CUtensorMap* tm, const int8_t* x, int64_t ld, int64_t m_pad) {
     return MI_OK;
 }
 
+// The packed words (m, nw) uint64 as a 2-D TMA tensor for the word-operand
+// build: 16-word (4 k-block, 128-byte) x 128-column boxes, 128-byte swizzle,
+// zero fill beyond nw and m.  The row pitch nw * 8 must be a multiple of 16.
+int make_tmap_words(CUtensorMap* tm, const uint64_t* words, int64_t nw, int64_t m) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc;
+    int rc = get_encode(&enc);
+    if (rc) return rc;
+    cuuint64_t gdim[2] = {(cuuint64_t)nw, (cuuint64_t)m};
+    cuuint64_t gstride[1] = {(cuuint64_t)nw * 8};
+    cuuint32_t box[2] = {16, 128};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(words), gdim, gstride, box, estride,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MI_ERR_CUDA, "cuTensorMapEncodeTiled (words) failed (CUresult %d)", (int)r);
+    return MI_OK;
+}
+
 // rcp = round(2^(62 + nb) / N) and off0 = -(nb - 2) - s for fixed_to_fp
 void fixed_point_consts(int64_t N, unsigned long long* rcp, int* off0) {
     int nb = 0;
@@ -236,6 +254,30 @@ int mi_gram_mi(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, in
                const int32_t* d_tiles, int64_t n_tiles, void* stream) {
     return launch_fused(d_kmajor, d_colstat, n_rows, n_cols, ld, mode, epsilon, include_diagonal, out_kind, d_out,
                         ld_out, d_tiles, n_tiles, nullptr, (cudaStream_t)stream);
+}
+
+int mi_gram_mi_words(const uint64_t* d_words, const void* d_colstat, int64_t n_rows, int64_t n_cols, int mode,
+                     double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
+                     const int32_t* d_tiles, int64_t n_tiles, void* stream) {
+    if (!d_words || !d_colstat) return fail(MI_ERR_DOMAIN, "d_words and d_colstat are required");
+    return launch_fused(nullptr, d_colstat, n_rows, n_cols, 0, mode, epsilon, include_diagonal, out_kind, d_out, ld_out,
+                        d_tiles, n_tiles, nullptr, (cudaStream_t)stream, d_words);
+}
+
+int mi_colstat_words(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, void* d_colstat, int32_t* d_colsum,
+                     void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (!d_words || !d_colstat) return fail(MI_ERR_DOMAIN, "d_words and d_colstat are required");
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    const int64_t nw = (n_rows + 63) / 64;
+    // kernel 1 without the expansion (x = nullptr): column sums + statistics only
+    MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, nw, nullptr, mi_kmajor_ld(n_rows), mi_kmajor_rows(n_cols),
+                                 d_colsum, (ColStat*)d_colstat, xlogx_ptr(d_colstat, n_rows, n_cols),
+                                 blkrange_ptr(d_colstat, n_rows, n_cols), fixr_ptr(d_colstat, n_rows, n_cols),
+                                 operand_fp4(n_rows), nullptr, mi_tile_size(), info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
 }
 
 int mi_scatter_tiles(const void* d_src, const int32_t* d_tiles, int64_t n_tiles, int64_t n_cols, int esz, void* d_dst,
@@ -346,11 +388,15 @@ int mi_unpermute(const void* d_in, int64_t ld_in, void* d_out, int64_t ld_out, i
 
 int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
                  double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const int32_t* d_tiles,
-                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream) {
+                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream, const uint64_t* d_words) {
     int rc = check_shape(n_rows, n_cols);
     if (rc) return rc;
     if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
-    if (ld < mi_kmajor_ld(n_rows) || ld % 128)
+    // d_words: the word-operand build (expansion in the producer; no X, no TMA)
+    const bool xp = d_words != nullptr;
+    if (xp && !operand_fp4(n_rows))
+        return fail(MI_ERR_DOMAIN, "the word-operand build needs e2m1 operands (n_rows < 2^24, SM-pair tiles)");
+    if (!xp && (ld < mi_kmajor_ld(n_rows) || ld % 128))
         return fail(MI_ERR_DIMENSION, "ld %lld must be a multiple of 128 and >= %lld", (long long)ld,
                     (long long)mi_kmajor_ld(n_rows));
     if (ld_out != MI_PACKED_UPPER && ld_out != MI_TILE_MAJOR && ld_out < n_cols)
@@ -361,13 +407,18 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     if (n_tiles == 0) return MI_OK;
     if (out_kind == MI_OUT_COUNTS && mode != MI_MODE_EXACT)
         return fail(MI_ERR_DOMAIN, "counts export ignores the mode; pass MI_MODE_EXACT");
-    if ((reinterpret_cast<uintptr_t>(d_kmajor) & 15) != 0)
+    if (xp && ((reinterpret_cast<uintptr_t>(d_words) & 15) != 0 || ((n_rows + 63) / 64) % 2 != 0))
+        return fail(MI_ERR_DOMAIN, "the word-operand build needs 16-byte aligned words and an even word count per column");
+    if (!xp && (reinterpret_cast<uintptr_t>(d_kmajor) & 15) != 0)
         return fail(MI_ERR_DOMAIN, "kmajor operand must be 16-byte aligned");
     DevInfo info;
     if ((rc = current_device_info(&info))) return rc;
     CUtensorMap tm;
-    if ((rc = make_tmap(&tm, d_kmajor, ld, mi_kmajor_rows(n_cols)))) return rc;
+    if (!xp && (rc = make_tmap(&tm, d_kmajor, ld, mi_kmajor_rows(n_cols)))) return rc;
+    if (xp && (rc = make_tmap_words(&tm, d_words, (n_rows + 63) / 64, n_cols))) return rc;
     GramMiParams p;
+    p.words = d_words;
+    p.nw = (n_rows + 63) / 64;
     p.colstat = reinterpret_cast<const ColStat*>(d_colstat);
     p.tiles = reinterpret_cast<const int2*>(d_tiles);
     p.n_tiles = (int)n_tiles;
@@ -389,7 +440,7 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     p.evac = tuning().evac;
     p.serp = tuning().serp;
     p.pace = nullptr;
-    p.pace_window = pace_window(n_tiles, p.num_k_blocks, info.num_sms);
+    p.pace_window = xp ? 0 : pace_window(n_tiles, p.num_k_blocks, info.num_sms);
     if (p.pace_window > 0 && (rc = pace_slots(dev, &p.pace))) return rc;
     const TailPlan tp = tail_plan(n_tiles, cta_group(), info.num_sms / cta_group(), p.num_k_blocks);
     p.n_full = tp.n_full;
@@ -422,8 +473,11 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     p.f32_epi = (tuning().f32_epi && tuning().fixed != 0 && out_kind == MI_OUT_F32 && n_rows < kFp4MaxN) ? 1 : 0;
     int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
-    MI_CUDA(launch_gram_mi(cta_group(), operand_fp4(n_rows), out_kind, eff_mode, tuning().stages, tuning().epi_warps,
-                           tm, p, info.num_sms, stream));
+    if (xp)
+        MI_CUDA(launch_gram_mi_words(out_kind, eff_mode, tm, p, info.num_sms, stream));
+    else
+        MI_CUDA(launch_gram_mi(cta_group(), operand_fp4(n_rows), out_kind, eff_mode, tuning().stages,
+                               tuning().epi_warps, tm, p, info.num_sms, stream));
     if (tp.kmode) MI_CUDA(cudaEventRecord(g_tail_ev[dev], stream));
     return MI_OK;
 }

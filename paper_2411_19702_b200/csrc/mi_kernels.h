@@ -69,7 +69,16 @@ struct GramMiParams {
     int tail_epi;
     unsigned int* tail_flag;
     uint32_t* tail_part;
+    // Word-operand build (XP): the operands are expanded from the packed words
+    // (m, nw) by producer warps straight into the swizzled shared-memory
+    // stages; X never exists in HBM (tall-N / narrow-m shapes).
+    const uint64_t* words;
+    int64_t nw;
 };
+constexpr int kXpRowWarps = 4;          // word-operand build: warps covering one 128-row operand half
+constexpr int kXpWarps = 2 * kXpRowWarps;  // word-operand build: expander warps per CTA (two groups)
+constexpr int kXpEpiWarps = 4;          // word-operand build: epilogue warps
+constexpr int kXpStages = 4;            // word-operand build: operand ring depth (a raw-word ring sits in front)
 constexpr int kPaceStride = 8;          // u32 per cluster slot (one 32-B sector each)
 constexpr int kPaceMaxClusters = 256;
 constexpr int kTailMaxUnits = 148;      // split tail units (<= clusters): flag pairs and partial slots
@@ -81,6 +90,11 @@ constexpr long long kFp4MaxN = 1ll << 24;    // e2m1 operands: fp32 accumulators
 // fp4: operand X holds e2m1 nibbles (kind::mxf4 build, cg == 2 only), else int8 bytes
 cudaError_t launch_gram_mi(int cg, bool fp4, int out_kind, int mode, int stages, int epi_warps,
                            const CUtensorMap& tmap, const GramMiParams& p, int num_sms, cudaStream_t stream);
+// The word-operand build (p.words, p.nw; e2m1 operands expanded in the
+// producer, CTA pairs, 4 epilogue warps, unpaced).
+// tmap: the words (m, nw) uint64 as a 2-D tensor, 16 x 128 boxes, 128-byte swizzle
+cudaError_t launch_gram_mi_words(int out_kind, int mode, const CUtensorMap& tmap, const GramMiParams& p, int num_sms,
+                                 cudaStream_t stream);
 int gram_mi_tile_size(int cg);
 
 // block_mask (device, one byte per tile-size column block, or nullptr = all):

@@ -191,8 +191,10 @@ unpack_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, 
         for (int u = 0; u < kUnr; ++u) {
             if (active && kb + u < kb1) {
                 cnt += __popcll(wv[u]);
-                if constexpr (FP4) store_fp4_word(xc + (kb + u) * kb_stride, wv[u]);
-                else store_int8_word(xc + (kb + u) * kb_stride, wv[u]);
+                if (x) {  // x == nullptr: column sums only (the word-operand GEMM expands in its producer)
+                    if constexpr (FP4) store_fp4_word(xc + (kb + u) * kb_stride, wv[u]);
+                    else store_int8_word(xc + (kb + u) * kb_stride, wv[u]);
+                }
             }
         }
     }

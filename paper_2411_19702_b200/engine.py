@@ -79,17 +79,19 @@ _OUT_KIND = {torch.float64: nat.MI_OUT_F64, torch.float32: nat.MI_OUT_F32, torch
 
 @dataclass
 class Prepared:
-    """Device-resident operand of one dataset: K-major int8 X and column sums."""
+    """Device-resident operand of one dataset: K-major X (or, on the word-operand
+    path, the packed words themselves) and column sums."""
 
     n_rows: int
     n_cols: int
     ld: int          # bytes per X row (N_pad)
     m_pad: int       # X rows
-    x: torch.Tensor  # int8 (m_pad, ld)
+    x: torch.Tensor | None  # int8 (m_pad, ld); None on the word-operand path
     colsum: torch.Tensor  # int32 (m_pad,)
     colstat: torch.Tensor  # uint8 workspace (mi_colstat_bytes): marginals + their log2 splits
     perm: torch.Tensor | None = None  # order "colsum": int32 slot -> column (X, colsum, colstat in slot order)
     inv: torch.Tensor | None = None   # order "colsum": int32 column -> slot
+    words: torch.Tensor | None = None  # word-operand path: the (m, nw) words the GEMM expands itself
 
 
 ORDERS = ("natural", "colsum", "auto")
@@ -228,9 +230,17 @@ class MIEngine:
         lo, hi = (int(x) for x in spread.cpu())
         return "colsum" if hi - lo > nat.get_tuning("table_thr") else "natural"
 
-    def _alloc_prepared(self, n_rows: int, n_cols: int):
+    @staticmethod
+    def words_operand(n_rows: int, n_cols: int) -> bool:
+        """The C ABI's rule (mi_words_operand; knobs "xp", "xp_cols"): the
+        word-operand GEMM, which expands the packed words in its producer warps
+        so that X never reaches HBM, for narrow m (tall-N shapes, where the X
+        round trip costs as much as the MMAs)."""
+        return bool(nat.lib().mi_words_operand(n_rows, n_cols))
+
+    def _alloc_prepared(self, n_rows: int, n_cols: int, xp: bool = False):
         ld, m_pad = self.layout(n_rows, n_cols)
-        x = torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
+        x = None if xp else torch.empty((m_pad, ld), dtype=torch.int8, device=self.device)
         colsum = torch.empty((m_pad,), dtype=torch.int32, device=self.device)
         colstat = torch.empty((int(nat.lib().mi_colstat_bytes(n_rows, n_cols)),), dtype=torch.uint8, device=self.device)
         return x, colsum, colstat
@@ -250,7 +260,8 @@ class MIEngine:
         """Staged kernel 1, first part (mi_unpack_prep): buffers and the
         per-call prologue; then prepare_range() per column group as its words
         arrive (dispatch's staged broadcast)."""
-        x, colsum, colstat = self._alloc_prepared(n_rows, n_cols)
+        xp = self.words_operand(n_rows, n_cols)
+        x, colsum, colstat = self._alloc_prepared(n_rows, n_cols, xp)
         ld, m_pad = self.layout(n_rows, n_cols)
         nat.check(nat.lib().mi_unpack_prep(n_rows, n_cols, colstat.data_ptr(), _stream_ptr(self.device)),
                   "mi_unpack_prep")
@@ -262,9 +273,13 @@ class MIEngine:
         1) and their statistics (mi_unpack_colsum_range)."""
         self._check_words(words_dev, prep.n_rows, prep.n_cols)
         mask = self._rank_mask(prep.n_cols, rank, world)
-        nat.check(nat.lib().mi_unpack_colsum_range(words_dev.data_ptr(), prep.n_rows, prep.n_cols, prep.x.data_ptr(),
+        if prep.x is None:  # word-operand path: statistics only, the GEMM reads these words
+            prep.words = words_dev
+        nat.check(nat.lib().mi_unpack_colsum_range(words_dev.data_ptr(), prep.n_rows, prep.n_cols,
+                                                   prep.x.data_ptr() if prep.x is not None else None,
                                                    prep.ld, prep.colstat.data_ptr(), prep.colsum.data_ptr(),
-                                                   mask.data_ptr() if mask is not None else None, c_begin, c_end,
+                                                   mask.data_ptr() if mask is not None and prep.x is not None
+                                                   else None, c_begin, c_end,
                                                    _stream_ptr(self.device)),
                   "mi_unpack_colsum_range")
 
@@ -283,8 +298,15 @@ class MIEngine:
             order = self.choose_order(words_dev, n_rows, n_cols, world)
         if order == "colsum" and world > 1:
             raise DomainError("order='colsum' is single-GPU only (each rank would unpermute the whole matrix)")
-        x, colsum, colstat = self._alloc_prepared(n_rows, n_cols)
         ld, m_pad = self.layout(n_rows, n_cols)
+        if order == "natural" and self.words_operand(n_rows, n_cols):
+            # word-operand path: column statistics only; compute() expands the words in the GEMM
+            x, colsum, colstat = self._alloc_prepared(n_rows, n_cols, True)
+            nat.check(nat.lib().mi_colstat_words(words_dev.data_ptr(), n_rows, n_cols, colstat.data_ptr(),
+                                                 colsum.data_ptr(), _stream_ptr(self.device)),
+                      "mi_colstat_words")
+            return Prepared(n_rows, n_cols, ld, m_pad, None, colsum, colstat, words=words_dev)
+        x, colsum, colstat = self._alloc_prepared(n_rows, n_cols)
         mask = self._rank_mask(n_cols, rank, world)
         if order == "colsum":
             perm, inv = self.column_order(words_dev, n_rows, n_cols)
@@ -347,6 +369,14 @@ class MIEngine:
             ld_out = out.stride(0)
         if tiles is None:
             tiles = self.tiles(m)
+        if prep.x is None:
+            if prep.words is None:
+                raise DomainError("word-operand prepare without words (prepare_range was not called)")
+            nat.check(nat.lib().mi_gram_mi_words(prep.words.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m,
+                                                 mode, eps, diag, kind, out.data_ptr(), ld_out,
+                                                 tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),
+                      "mi_gram_mi_words")
+            return out
         nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m, prep.ld,
                                        mode, eps, diag, kind, out.data_ptr(), ld_out,
                                        tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),

@@ -149,6 +149,7 @@ KNOB_VARIANTS = [
     {"tail": 2}, {"tail": 3}, {"tail": 3, "cta_group": 1}, {"tail": 2, "cta_group": 1}, {"tail": 3, "pace": 16},
     {"fp4": 0}, {"fp4": 0, "tail": 3}, {"fp4": 0, "pace": 16}, {"fp4": 0, "fixed": 0},
     {"fixed": 3}, {"hybrid": 0}, {"fixed": 3, "fp4": 0}, {"serp": 1}, {"serp": 1, "pace": 16},
+    {"xp": 0}, {"xp": 1}, {"xp": 1, "tail": 3}, {"xp": 1, "tail": 2}, {"xp": 1, "fixed": 0}, {"xp": 1, "evac": 0},
 ]
 
 
