@@ -64,7 +64,7 @@ Tuning& tuning() {
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
                        env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1), env_int("MI_B200_XP", -1),
-                       env_int("MI_B200_XP_COLS", 2048)};
+                       env_int("MI_B200_XP_COLS", 3072)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }

@@ -203,6 +203,38 @@ unpack_direct_kernel(const uint64_t* __restrict__ words, int64_t m, int64_t nw, 
     if (j == 0 && real && cnt) atomicAdd(&colstat[c].vi, (int)cnt);
 }
 
+// Column sums only (the word-operand path: its GEMM expands the words itself,
+// so kernel 1 just counts).  Each warp owns a contiguous chunk of one
+// column's words -- kColsumChunk words, 8 loads of 8 bytes in flight per lane,
+// 256 contiguous bytes per warp load -- and adds its popcount to the column's
+// counter: a streaming read of the words at full DRAM efficiency.
+constexpr int kColsumChunk = 2048;
+__global__ void __launch_bounds__(256) colsum_words_kernel(const uint64_t* __restrict__ words, int64_t m,
+                                                           int64_t nw, int64_t c_begin, int64_t c_end,
+                                                           ColStat* __restrict__ colstat) {
+    const int lane = threadIdx.x & 31;
+    const int64_t chunks = (nw + kColsumChunk - 1) / kColsumChunk;
+    const int64_t cols = (c_end < m ? c_end : m) - c_begin;
+    const int64_t units = cols * chunks;
+    for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; u < units;
+         u += (int64_t)gridDim.x * blockDim.x / 32) {
+        const int64_t c = c_begin + u / chunks;
+        const int64_t w0 = (u % chunks) * kColsumChunk;
+        const int64_t w1 = w0 + kColsumChunk < nw ? w0 + kColsumChunk : nw;
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(words + c * nw);
+        uint32_t cnt = 0;
+        for (int64_t w = w0 + lane; w < w1; w += 32 * 8) {
+            unsigned long long v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = w + 32 * k < w1 ? __ldcs(src + w + 32 * k) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cnt += __popcll(v[k]);
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0 && cnt) atomicAdd(&colstat[c].vi, (int)cnt);
+    }
+}
+
 // Epilogue of kernel 1: per-column statistics from the finished counts.
 __global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m, int64_t c_begin, int64_t c_end,
                                                       int32_t* __restrict__ colsum, ColStat* __restrict__ colstat,
@@ -231,7 +263,14 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
                                 cudaStream_t stream, const int32_t* perm) {
     if (c_begin % kUnpackCols || c_end % kUnpackCols || c_end > m_pad || c_begin >= c_end) return cudaErrorInvalidValue;
     const int fix_s = xlogx_scale(n_rows);
-    {
+    if (!x) {  // statistics only: a streaming popcount of the columns' words
+        const int64_t chunks = (nw + kColsumChunk - 1) / kColsumChunk;
+        const int64_t cols = (c_end < m ? c_end : m) - c_begin;
+        int64_t blocks = (cols * chunks + 7) / 8;
+        if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+        if (blocks > 0)
+            colsum_words_kernel<<<(unsigned)blocks, 256, 0, stream>>>(words, m, nw, c_begin, c_end, colstat);
+    } else {
         // tools/unpack_bench.py sweeps (r01h, r01m): 32 k-blocks per block and 16
         // loads in flight per thread were best across configs 3-5 (the kernel
         // is memory-latency bound at 50% occupancy: ncu long-scoreboard stalls)

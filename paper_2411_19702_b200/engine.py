@@ -92,6 +92,16 @@ class Prepared:
     perm: torch.Tensor | None = None  # order "colsum": int32 slot -> column (X, colsum, colstat in slot order)
     inv: torch.Tensor | None = None   # order "colsum": int32 column -> slot
     words: torch.Tensor | None = None  # word-operand path: the (m, nw) words the GEMM expands itself
+    layout_knobs: tuple = ()  # ("fp4", "cta_group") at prepare time: X's format depends on them
+
+    def __post_init__(self):
+        if not self.layout_knobs:
+            self.layout_knobs = _layout_knobs()
+
+
+def _layout_knobs() -> tuple:
+    """The knobs that fix the operand format (e2m1 or int8 X, tile size)."""
+    return (nat.get_tuning("fp4"), nat.get_tuning("cta_group"))
 
 
 ORDERS = ("natural", "colsum", "auto")
@@ -338,6 +348,9 @@ class MIEngine:
         if kind == nat.MI_OUT_COUNTS:
             mode = nat.MI_MODE_EXACT
         m = prep.n_cols
+        if prep.layout_knobs != _layout_knobs():
+            raise DomainError("the fp4 / cta_group knobs changed between prepare() and compute(): "
+                              f"X was laid out for {prep.layout_knobs}, the kernel would read {_layout_knobs()}")
         if prep.perm is not None:
             if tile_major:
                 raise DomainError("order='colsum' computes the full matrix: no tile-major output")

@@ -113,7 +113,9 @@ def test_output_forms_and_tile_subsets(engine):
         full = engine.compute(prep, None, torch.float64).cpu().numpy()
         packed = engine.compute(prep, None, torch.float64, packed=True).cpu().numpy()
         tl = engine.tiles(m, 1, 3)
-        shard = engine.compute(prep, None, torch.float32, tiles=tl, tile_major=True).cpu().numpy()
+        # (cells past m in the last block are never written: start from zeros)
+        shard = torch.zeros((int(tl.shape[0]), 256, 256), dtype=torch.float32, device=engine.device)
+        shard = engine.compute(prep, None, torch.float32, tiles=tl, tile_major=True, out=shard).cpu().numpy()
         return full, packed, shard
 
     a, b = both_paths(engine, words, n, run)
@@ -169,3 +171,18 @@ def test_default_rule_picks_words_for_narrow_m(engine):
         assert engine.words_operand(102_400, 2048)
         assert not engine.words_operand(100_000, 10_000)
         assert not engine.words_operand((1 << 24) + 1, 256)  # int8 operands: no word build
+
+
+def test_layout_knob_change_between_prepare_and_compute_is_rejected(engine):
+    """X's format is fixed by the fp4 / cta_group knobs at prepare time; a
+    compute() under other knobs would read it wrongly, so it raises."""
+    from paper_2411_19702_b200 import DomainError
+
+    n, m = 5000, 5000  # the unpack path (m_pad > xp_cols)
+    rng = np.random.default_rng(3)
+    w = engine.upload(O.pack_bits(rand_bits(rng, n, m, 0.5)))
+    prep = engine.prepare(w, n, m)
+    with knobs(fp4=0):
+        with pytest.raises(DomainError):
+            engine.compute(prep, None, torch.float64)
+    engine.compute(prep, None, torch.float64)  # unchanged knobs: fine
