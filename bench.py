@@ -62,6 +62,7 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-dropin", action="store_true", help="skip the drop-in mi_all_pairs (numpy) e2e variant")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-tall-narrow", action="store_true", help="skip the tall-N / narrow-m section")
     p.add_argument("--sustained-seconds", type=float, default=2.0)
     p.add_argument("--stages", type=int, default=-1, help="staged-broadcast column groups (-1 auto)")
     p.add_argument("--plumbing-check", action="store_true",
@@ -504,6 +505,13 @@ def run_gpu(args):
     if not args.no_e2e:
         e2e = run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W, stages, buf)
 
+    tall = None
+    if rank == 0 and world == 1 and not args.no_tall_narrow:
+        try:
+            tall = run_tall_narrow(eng, peak)
+        except Exception as exc:  # a side measurement must never sink the headline
+            tall = {"error": str(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -532,12 +540,82 @@ def run_gpu(args):
                                       "once (NCCL)" if world > 1 else "1 GPU",
                        "l2": "flushed between steps (256 MiB write, untimed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "sustained": sustained, "clocks": clocks,
+            "tall_narrow": tall,
             "comm": comm, "gpu_launches": launches * args.steps,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def hbm_peak_gbs():
+    """Measured HBM bandwidth of this pool's B200s (MEASURED_PEAKS.json), else
+    the profiling guide's fallback."""
+    f = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(f.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy read+write)"
+    except Exception:
+        return 6500.0, "fallback 6500 GB/s"
+
+
+def run_tall_narrow(eng, tensor_peak_tops, n=8_000_000, m=512, reps=10):
+    """The north_star's tall-N / narrow-m case (reading D dominates): one
+    step = column statistics + fused Gram + MI on device-resident words,
+    float64 MI, both operand paths -- the word-operand build (expansion in the
+    GEMM's producer warps, X never in HBM; the default for this shape) and the
+    unpack + TMA build (X written to HBM and read back) -- CUDA events, L2
+    flushed between reps, bit-identity of the two results checked."""
+    import torch
+
+    from paper_2411_19702_b200 import datagen
+    from paper_2411_19702_b200 import _native as nat
+
+    dev = eng.device
+    w = datagen.generate(n, m, 0.3, 11, dev)
+    out = torch.empty((m, m), dtype=torch.float64, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    W = pair_samples(n, m)
+    words_b, mi_b = w.numel() * 8, m * m * 8
+    hbm, hbm_src = hbm_peak_gbs()
+    res, mats = {}, {}
+    old = nat.get_tuning("xp")
+    try:
+        for xp in (1, 0):
+            nat.set_tuning(xp=xp)
+            run = lambda: eng.compute(eng.prepare(w, n, m), None, torch.float64, out=out)
+            run()
+            torch.cuda.synchronize()
+            mats[xp] = out.clone()
+            ts, tk = [], []
+            for _ in range(reps):
+                flush.fill_(1)
+                a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                a.record(stream)
+                prep = eng.prepare(w, n, m)
+                b.record(stream)
+                eng.compute(prep, None, torch.float64, out=out)
+                c.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(c))
+                tk.append(b.elapsed_time(c))
+                del prep
+            step, kern = statistics.median(ts), statistics.median(tk)
+            key = "words_operand" if xp else "unpack_tma"
+            res[key] = {"step_ms": step, "fused_ms": kern, "value": W / (step * 1e-3),
+                        "algorithmic_gbs": (words_b + mi_b) / (step * 1e-3) / 1e9,
+                        "tensor_frac_of_peak": 2 * W / (kern * 1e-3) / 1e12 / tensor_peak_tops}
+    finally:
+        nat.set_tuning(xp=old)
+    return {"workload": f"N={n:,} x m={m} Bernoulli(0.3), float64 MI, device-resident words", "unit": UNIT,
+            "words_bytes": words_b, "mi_bytes": mi_b, "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
+            "default_path": "words_operand" if eng.words_operand(n, m) else "unpack_tma",
+            "bit_identical": bool(torch.equal(mats[0], mats[1])),
+            "speedup_words_over_unpack": res["unpack_tma"]["step_ms"] / res["words_operand"]["step_ms"],
+            "roofline_note": "tensor work 2W counts m(m+1)/2 pairs; the 256-wide diagonal tiles compute 1.5x that "
+                             "at m = 512, so the MMA-issue ceiling is ~0.67 of peak",
+            **res}
 
 
 def run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W, stages, buf):
