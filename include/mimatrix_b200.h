@@ -153,6 +153,17 @@ int mi_colstat_words(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, vo
 int mi_gram_mi_words(const uint64_t* d_words, const void* d_colstat, int64_t n_rows, int64_t n_cols, int mode,
                      double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out,
                      const int32_t* d_tiles, int64_t n_tiles, void* stream);
+/* mi_gram_mi_words that also computes the column statistics into d_colstat
+ * (and the column sums into d_colsum, if not NULL): no mi_colstat_words
+ * first.  With the full tile list of a narrow matrix (every tile a K-range
+ * tail unit: the default schedule when the tiles are fewer than the SM pairs)
+ * it is ONE fused launch that reads the words once -- the expander warps count
+ * the ones of each column on the diagonal tiles' units and the epilogue warps
+ * build the statistics while the units run ("xp_stats" knob, default 1);
+ * otherwise kernel 1's counting pass runs first. */
+int mi_gram_mi_words_stats(const uint64_t* d_words, void* d_colstat, int32_t* d_colsum, int64_t n_rows,
+                           int64_t n_cols, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
+                           int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream);
 /* binmat.from_bits / from_rows (binmat.py:34-46,136-172) on the device: a
  * row-major uint8 0/1 matrix (n_rows x n_cols, row pitch ld_bits bytes) ->
  * the words layout (n_cols x ceil(n_rows/64) uint64, padding bits zero).

@@ -75,6 +75,7 @@ SIGNATURES = {
     "mi_words_operand": (_int, [_i64, _i64]),
     "mi_colstat_words": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "mi_gram_mi_words": (_int, [_vp, _vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
+    "mi_gram_mi_words_stats": (_int, [_vp, _vp, _vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _i64, _vp, _i64, _vp]),
     "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
     "mi_all_pairs_host_packed": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),

@@ -64,7 +64,7 @@ Tuning& tuning() {
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
                        env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1), env_int("MI_B200_XP", -1),
-                       env_int("MI_B200_XP_COLS", 3072)};
+                       env_int("MI_B200_XP_COLS", 3072), env_int("MI_B200_XP_STATS", 1)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -271,6 +271,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "xp")) {
         if (value < -1 || value > 1) return fail(MI_ERR_DOMAIN, "xp must be -1 (auto), 0 (off) or 1 (on)");
         t.xp = value;
+    } else if (!strcmp(key, "xp_stats")) {
+        if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "xp_stats must be 0 or 1");
+        t.xp_stats = value;
     } else if (!strcmp(key, "xp_cols")) {
         if (value < 0) return fail(MI_ERR_DOMAIN, "xp_cols must be >= 0");
         t.xp_cols = value;
@@ -308,6 +311,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "xp")) return t.xp;
     if (!strcmp(key, "debug")) return t.debug;
     if (!strcmp(key, "xp_cols")) return t.xp_cols;
+    if (!strcmp(key, "xp_stats")) return t.xp_stats;
     return -1;
 }
 

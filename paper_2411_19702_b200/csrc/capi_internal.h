@@ -26,7 +26,7 @@ constexpr int kMaxIngestStages = 16;
 int env_int(const char* name, int dflt);
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid, unperm_ctas, ingest, ingest_split, serp, f32_epi, xp, xp_cols;
+        hybrid, unperm_ctas, ingest, ingest_split, serp, f32_epi, xp, xp_cols, xp_stats;
 };
 // the word-operand build (mi_words_operand's rule)
 bool words_operand(int64_t n_rows, int64_t n_cols);
@@ -67,7 +67,8 @@ struct TailPlan {
 TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb);
 int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
                  double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const int32_t* d_tiles,
-                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream, const uint64_t* d_words = nullptr);
+                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream, const uint64_t* d_words = nullptr,
+                 bool stats = false, int32_t* d_colsum = nullptr);
 
 }  // namespace capi
 }  // namespace mib200

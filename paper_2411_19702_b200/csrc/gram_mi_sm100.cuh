@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "colstat.cuh"
 #include "milog.cuh"
 #include "mi_kernels.h"
 #include "ptx.cuh"
@@ -925,6 +926,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 // = its position in this CTA's k-block sequence modulo ST.
                 const int xw = warp - C::PACER_WARP - 1;
                 const int grp = xw / kXpRowWarps;
+                const int m_real = p.m;
                 const int xt = (xw % kXpRowWarps) * 32 + (int)lane;
                 const uint32_t full_leader0 = map_to_cta(full_bar(0), 0u);
                 const uint32_t sw = (uint32_t)xt & 7u;
@@ -936,6 +938,9 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     int ra0, rb0, kb0, kb1;
                     bool share;
                     seg(sg, ra0, rb0, kb0, kb1, share);
+                    // statistics mode: diagonal units count their columns' ones
+                    const bool count = p.xp_stats && share;
+                    uint32_t ones = 0;
                     for (int q = kb0 / kXpKbPerRaw; q <= (kb1 - 1) / kXpKbPerRaw; ++q) {
                         const int lo = max(kb0, q * kXpKbPerRaw), hi = min(kb1, (q + 1) * kXpKbPerRaw);
                         const int my0 = max(lo, q * kXpKbPerRaw + 2 * grp), my1 = min(hi, q * kXpKbPerRaw + 2 * grp + 2);
@@ -963,6 +968,13 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                                         lds128(rowa + kXpRawHalfBytes + (((2u * jj + 1u) ^ sw) << 4), wb[i][2], wb[i][3]);
                                     }
                                 }
+                            }
+                            if (count) {
+#pragma unroll
+                                for (int i = 0; i < 2; ++i)
+                                    if (i == 0 || two)
+                                        ones += __popcll(wa[i][0]) + __popcll(wa[i][1]) + __popcll(wa[i][2]) +
+                                                __popcll(wa[i][3]);
                             }
                             const long long t1 = xtr ? clock64() : 0;
                             xwait(empty_bar(s0), p0 ^ 1u);
@@ -1004,6 +1016,12 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                         if (++r == L::RS) { r = 0; rph ^= 1u; }
                         ctr += hi - lo;
                     }
+                    if (count) {  // publish this warp's counts of the segment (its k-blocks, its rows)
+                        if (ra0 + xt < m_real && ones) atomicAdd(&p.colstat_w[ra0 + xt].vi, (int)ones);
+                        __threadfence();
+                        __syncwarp();
+                        if (lane == 0) atomicAdd(p.xp_sync, 1u);
+                    }
                 }
                 if (xtr && xw == 0 && lane == 0)
                     for (int k = 0; k < 6; ++k) xtr[8 * rank + k] = acc_t[k];
@@ -1037,6 +1055,45 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         }
     } else {
         // ================= epilogue =================
+        if constexpr (XP) {
+            if (p.xp_stats) {
+                // statistics mode: while the units run, build the T table, then wait
+                // for the diagonal units' column counts, write the column statistics
+                // (a slice per thread across the grid) and meet every CTA at a
+                // grid-wide barrier (all CTAs are co-resident: one per SM)
+                const long long gtid = (long long)blockIdx.x * (EW * 32) + etid;
+                const long long gthreads = (long long)gridDim.x * (EW * 32);
+                if (p.xlogx_w)
+                    for (long long c = gtid; c <= p.n_rows; c += gthreads)
+                        p.xlogx_w[c] = fix_xlog2x((unsigned)c, p.fix_s, kFixR, kFixLG);
+                volatile unsigned int* sync = p.xp_sync;
+                if (etid == 0) {
+                    const long long t0 = clock64();
+                    while (sync[0] < p.xp_diag_expect) {
+                        __nanosleep(256);
+                        if (clock64() - t0 > (1ll << 36)) __trap();  // a lost unit is a bug
+                    }
+                    __threadfence();
+                }
+                named_barrier_sync(5, EW * 32);
+                const int64_t m_pad = (int64_t)((p.m + C::TS - 1) / C::TS) * C::TS;
+                for (long long c = gtid; c < m_pad; c += gthreads)  // whole warps: m_pad, gthreads are multiples of 32
+                    write_colstat(c, (uint32_t)__ldcg(&p.colstat_w[c].vi), p.n_rows, c < p.m, p.fix_s, p.colsum,
+                                  p.colstat_w, p.blkrange_w);
+                __threadfence();
+                named_barrier_sync(5, EW * 32);
+                if (etid == 0) {
+                    atomicAdd(p.xp_sync + 1, 1u);
+                    const long long t0 = clock64();
+                    while (sync[1] < gridDim.x) {
+                        __nanosleep(256);
+                        if (clock64() - t0 > (1ll << 36)) __trap();
+                    }
+                    __threadfence();
+                }
+                named_barrier_sync(5, EW * 32);
+            }
+        }
         const int q = warp & 3;                          // TMEM lane quadrant of this warp
         const int part = (warp - kEpiWarp0) >> 2;        // which column slice of the accumulator
         const int row_local = q * 32 + (int)lane;

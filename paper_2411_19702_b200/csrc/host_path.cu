@@ -225,8 +225,10 @@ int egress_buffer(Workspace& ws, size_t bytes, void** out) {
     return MI_OK;
 }
 
+// defer_stats: on the word-operand path leave the column statistics to
+// run_fused (computed inside the fused launch); otherwise kernel 1 does them.
 int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int64_t* ld_out,
-                 int64_t* m_pad_out, const DevInfo& info) {
+                 int64_t* m_pad_out, const DevInfo& info, bool defer_stats = false) {
     const int64_t nw = (n_rows + 63) / 64;
     const int64_t ld = mi_kmajor_ld(n_rows);
     const int64_t m_pad = mi_kmajor_rows(n_cols);
@@ -238,6 +240,9 @@ int stage_inputs(Workspace& ws, const uint64_t* h_words, int64_t n_rows, int64_t
     if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4)))) return rc;
     if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
     if ((rc = upload_words(ws, h_words, n_cols, nw))) return rc;
+    *ld_out = ld;
+    *m_pad_out = m_pad;
+    if (xp && defer_stats) return MI_OK;  // the word-operand launch computes them (run_fused)
     MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, xp ? nullptr : (int8_t*)ws.x, ld, m_pad,
                                  (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
                                  blkrange_ptr(ws.colstat, n_rows, n_cols), fixr_ptr(ws.colstat, n_rows, n_cols),
@@ -262,9 +267,11 @@ int workspace_for(int device, Workspace** out, DevInfo* info) {
     return MI_OK;
 }
 
+// stats: the inputs were staged with defer_stats (word-operand path: the
+// launch computes the column statistics too)
 int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t m_pad, int mode, double eps,
               int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const DevInfo& info,
-              unsigned int* row_done = nullptr) {
+              unsigned int* row_done = nullptr, bool stats = false) {
     (void)m_pad;
     const int64_t n_tiles = mi_num_tiles(n_cols);
     std::vector<int32_t> tiles = all_tiles(tiles_per_side(n_cols), tile_band(), row_done ? 1 : 0);
@@ -275,7 +282,7 @@ int run_fused(Workspace& ws, int64_t n_rows, int64_t n_cols, int64_t ld, int64_t
     const bool xp = words_operand(n_rows, n_cols);
     return launch_fused(xp ? nullptr : (const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps, include_diagonal,
                         out_kind, d_out, ld_out, (const int32_t*)ws.tiles, n_tiles, row_done, ws.stream,
-                        xp ? (const uint64_t*)ws.words : nullptr);
+                        xp ? (const uint64_t*)ws.words : nullptr, xp && stats, xp ? (int32_t*)ws.colsum : nullptr);
 }
 
 }  // namespace capi
@@ -505,7 +512,7 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
         return rc;
     }
     int64_t ld, m_pad;
-    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info, true))) return rc;
     stamp("H2D + unpack enqueued");
     const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
     const size_t row_bytes = (size_t)n_cols * esz;
@@ -548,7 +555,7 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
         for (int64_t k = 0; k < nt; ++k) expect[(size_t)tl[2 * k]] += cg * (k >= tp.n_full ? (unsigned)tp.epi : 1u);
     }
     if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out,
-                        packed ? MI_PACKED_UPPER : n_cols, info, ws->row_done_d)))
+                        packed ? MI_PACKED_UPPER : n_cols, info, ws->row_done_d, true)))
         return rc;
     stamp("fused kernel enqueued");
     // Stream finished rows to the host while the GEMM continues: rows of tile
@@ -617,11 +624,11 @@ int mi_gram_ones_host(const uint64_t* h_words, int64_t n_cols, int64_t n_words, 
     int rc;
     if ((rc = workspace_for(device, &ws, &info))) return rc;
     int64_t ld, m_pad;
-    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info))) return rc;
+    if ((rc = stage_inputs(*ws, h_words, n_rows, n_cols, &ld, &m_pad, info, true))) return rc;
     const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * 4;
     if ((rc = ensure(&ws->out, &ws->out_cap, out_bytes))) return rc;
     if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, MI_MODE_EXACT, 1e-12, 1, MI_OUT_COUNTS, ws->out, n_cols,
-                        info)))
+                        info, nullptr, true)))
         return rc;
     std::vector<int32_t> tmp((size_t)n_cols * (size_t)n_cols);
     MI_CUDA(cudaMemcpyAsync(tmp.data(), ws->out, out_bytes, cudaMemcpyDeviceToHost, ws->stream));

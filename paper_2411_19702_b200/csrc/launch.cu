@@ -105,6 +105,15 @@ int tail_slots(int device, unsigned int** flag, uint32_t** part) {
     return MI_OK;
 }
 
+std::mutex g_xp_mu;
+unsigned int* g_xp_sync[64] = {};
+int xp_sync_slots(int device, unsigned int** out) {
+    std::lock_guard<std::mutex> lk(g_xp_mu);
+    if (!g_xp_sync[device]) MI_CUDA(cudaMalloc((void**)&g_xp_sync[device], 64));
+    *out = g_xp_sync[device];
+    return MI_OK;
+}
+
 int pace_slots(int device, unsigned int** out) {
     std::lock_guard<std::mutex> lk(g_pace_mu);
     if (!g_pace[device]) {
@@ -264,6 +273,14 @@ int mi_gram_mi_words(const uint64_t* d_words, const void* d_colstat, int64_t n_r
                         d_tiles, n_tiles, nullptr, (cudaStream_t)stream, d_words);
 }
 
+int mi_gram_mi_words_stats(const uint64_t* d_words, void* d_colstat, int32_t* d_colsum, int64_t n_rows,
+                           int64_t n_cols, int mode, double epsilon, int include_diagonal, int out_kind, void* d_out,
+                           int64_t ld_out, const int32_t* d_tiles, int64_t n_tiles, void* stream) {
+    if (!d_words || !d_colstat) return fail(MI_ERR_DOMAIN, "d_words and d_colstat are required");
+    return launch_fused(nullptr, d_colstat, n_rows, n_cols, 0, mode, epsilon, include_diagonal, out_kind, d_out, ld_out,
+                        d_tiles, n_tiles, nullptr, (cudaStream_t)stream, d_words, true, d_colsum);
+}
+
 int mi_colstat_words(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, void* d_colstat, int32_t* d_colsum,
                      void* stream) {
     int rc = check_shape(n_rows, n_cols);
@@ -388,7 +405,8 @@ int mi_unpermute(const void* d_in, int64_t ld_in, void* d_out, int64_t ld_out, i
 
 int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
                  double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const int32_t* d_tiles,
-                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream, const uint64_t* d_words) {
+                 int64_t n_tiles, unsigned int* row_done, cudaStream_t stream, const uint64_t* d_words, bool stats,
+                 int32_t* d_colsum) {
     int rc = check_shape(n_rows, n_cols);
     if (rc) return rc;
     if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
@@ -473,6 +491,37 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     p.f32_epi = (tuning().f32_epi && tuning().fixed != 0 && out_kind == MI_OUT_F32 && n_rows < kFp4MaxN) ? 1 : 0;
     int eff_mode = out_kind == MI_OUT_COUNTS ? MI_MODE_EXACT : mode;
     // exact mode runs the FP64-free fixed-point epilogue whenever the table exists
+    // stats: this call computes the column statistics too -- inside the launch
+    // when every tile runs as K-range tail units (the expanders count the
+    // diagonal units' columns), else by kernel 1's counting pass first
+    p.xp_stats = 0;
+    p.xp_sync = nullptr;
+    p.xp_diag_expect = 0;
+    p.colstat_w = reinterpret_cast<ColStat*>(const_cast<void*>(d_colstat));
+    p.colsum = d_colsum;
+    p.blkrange_w = blkrange_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+    p.xlogx_w = nullptr;
+    if (stats) {
+        ColStat* cs = reinterpret_cast<ColStat*>(const_cast<void*>(d_colstat));
+        long long* xl = xlogx_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+        int2* br = blkrange_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+        float* fr = fixr_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
+        const int64_t T = tiles_per_side(n_cols);
+        const bool fused_stats = xp && n_tiles == T * (T + 1) / 2 && tp.n_full == 0 && tp.kmode && tp.split > 1 &&
+                                 tuning().xp_stats;
+        if (fused_stats) {
+            if ((rc = xp_sync_slots(dev, &p.xp_sync))) return rc;
+            MI_CUDA(launch_unpack_prep(n_rows, mi_kmajor_rows(n_cols), cs, xl, br, fr, info.num_sms, stream, false));
+            MI_CUDA(cudaMemsetAsync(p.xp_sync, 0, 2 * sizeof(unsigned int), stream));
+            p.xp_stats = 1;
+            p.xp_diag_expect = (unsigned)(T * tp.split * cta_group() * kXpWarps);
+            p.xlogx_w = xl;
+        } else {
+            MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, (n_rows + 63) / 64, xp ? nullptr : (int8_t*)d_kmajor,
+                                         ld, mi_kmajor_rows(n_cols), d_colsum, cs, xl, br, fr, operand_fp4(n_rows),
+                                         nullptr, mi_tile_size(), info.num_sms, stream));
+        }
+    }
     if (xp)
         MI_CUDA(launch_gram_mi_words(out_kind, eff_mode, tm, p, info.num_sms, stream));
     else

@@ -74,6 +74,19 @@ struct GramMiParams {
     // stages; X never exists in HBM (tall-N / narrow-m shapes).
     const uint64_t* words;
     int64_t nw;
+    // XP statistics mode (the tall-N step in one launch; all-tail K-range
+    // schedules with every tile): the expanders count the ones of each column
+    // on the diagonal tiles' units (they read every word of those columns
+    // exactly once) into colstat[c].vi, and the epilogue warps -- idle until
+    // the units finish -- build the T table, wait for the counts, write the
+    // column statistics and meet at a grid-wide barrier before any epilogue.
+    int xp_stats;
+    unsigned int* xp_sync;        // [0] diagonal expander-warp completions, [1] CTAs done (zeroed by the host)
+    unsigned int xp_diag_expect;  // completions [0] must reach
+    ColStat* colstat_w;           // writable alias of colstat
+    int32_t* colsum;              // optional column-sum output
+    int2* blkrange_w;             // writable alias of blkrange
+    long long* xlogx_w;           // the T table to build (or nullptr: none)
 };
 constexpr int kXpRowWarps = 4;          // word-operand build: warps covering one 128-row operand half
 constexpr int kXpWarps = 2 * kXpRowWarps;  // word-operand build: expander warps per CTA (two groups)
@@ -110,8 +123,9 @@ cudaError_t launch_unpack_colsum(const uint64_t* words, int64_t n_rows, int64_t 
 // block ranges, the fixed-point table) once, then the expansion + column
 // statistics of columns [c_begin, c_end) (c_begin a multiple of 32, c_end <=
 // m_pad) as their words arrive.  blkrange = nullptr when there is no table.
+// table = false: everything but the T table (the word-operand statistics mode builds it in the fused launch)
 cudaError_t launch_unpack_prep(int64_t n_rows, int64_t m_pad, ColStat* colstat, long long* xlogx, int2* blkrange,
-                               float* fixr, int num_sms, cudaStream_t stream);
+                               float* fixr, int num_sms, cudaStream_t stream, bool table = true);
 cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m, int64_t nw, int8_t* x, int64_t ld,
                                 int64_t m_pad, int32_t* colsum, ColStat* colstat, int2* blkrange, bool fp4,
                                 const uint8_t* block_mask, int tile, int64_t c_begin, int64_t c_end, int num_sms,

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "colstat.cuh"
 #include "mi_kernels.h"
 #include "milog.cuh"
 
@@ -55,50 +56,6 @@ __global__ void __launch_bounds__(256) unpack_prep_kernel(ColStat* __restrict__ 
     }
     __syncthreads();
     for (long long c = tid; c <= N; c += nthr) T[c] = fix_xlog2x((unsigned)c, s, R, LG);
-}
-
-// Per-column statistics for the fused epilogue (lane/thread owning column c).
-__device__ __forceinline__ void write_colstat(int64_t c, uint32_t cnt, int64_t n_rows, bool real, int fix_s,
-                                              int32_t* __restrict__ colsum, ColStat* __restrict__ colstat,
-                                              int2* __restrict__ blkrange) {
-    if (colsum) colsum[c] = (int32_t)cnt;
-    // marginal logs for the fused epilogue: log2(v) and log2(N - v)
-    ColStat st;
-    const int64_t v0 = n_rows - (int64_t)cnt;
-    int e1 = 0, e0 = 0;
-    st.v = (double)cnt;
-    st.nv = (double)v0;
-    st.f1 = cnt > 0 ? log2_frac((double)cnt, kLog2TabInit, e1) : 0.0;
-    st.f0 = v0 > 0 ? log2_frac((double)v0, kLog2TabInit, e0) : 0.0;
-    st.e1 = cnt > 0 ? (double)e1 : 0.0;
-    st.e0 = v0 > 0 ? (double)e0 : 0.0;
-    st.vi = (int)cnt;
-    st.pad = 0;
-    st.q = fix_xlog2x(cnt, fix_s, kFixR, kFixLG) + fix_xlog2x((unsigned)v0, fix_s, kFixR, kFixLG);
-    // float32 epilogue factors: N / a and 1 / a as float pairs (1.0 for a = 0)
-    const double dn = (double)n_rows;
-    auto split = [](double x, float& hi, float& lo) {
-        hi = (float)x;
-        lo = (float)(x - (double)hi);
-    };
-    st.f.v = (float)cnt;
-    split(cnt > 0 ? dn / (double)cnt : 1.0, st.f.s1h, st.f.s1l);
-    split(v0 > 0 ? dn / (double)v0 : 1.0, st.f.s0h, st.f.s0l);
-    split(cnt > 0 ? 1.0 / (double)cnt : 1.0, st.f.t1h, st.f.t1l);
-    split(v0 > 0 ? 1.0 / (double)v0 : 1.0, st.f.t0h, st.f.t0l);
-    st.f.pad[0] = st.f.pad[1] = st.f.pad[2] = 0.f;
-    colstat[c] = st;
-    if (blkrange) {
-        // per-128-column (min, max) of the real columns: one atomic pair per
-        // warp (its 32 columns lie in one block) instead of one per column
-        int lo = real ? (int)cnt : 0x7FFFFFFF, hi = real ? (int)cnt : -1;
-        lo = __reduce_min_sync(0xffffffffu, lo);
-        hi = __reduce_max_sync(0xffffffffu, hi);
-        if ((threadIdx.x & 31) == 0 && hi >= 0) {
-            atomicMin(&blkrange[c / 128].x, lo);
-            atomicMax(&blkrange[c / 128].y, hi);
-        }
-    }
 }
 
 // Column ranges of the staged launches start on multiples of 32.
@@ -245,15 +202,16 @@ __global__ void __launch_bounds__(256) colstat_kernel(int64_t n_rows, int64_t m,
 }
 
 cudaError_t launch_unpack_prep(int64_t n_rows, int64_t m_pad, ColStat* colstat, long long* xlogx, int2* blkrange,
-                               float* fixr, int num_sms, cudaStream_t stream) {
+                               float* fixr, int num_sms, cudaStream_t stream, bool table) {
     const int fix_s = xlogx_scale(n_rows);
-    int64_t work = xlogx ? n_rows + 1 : 0;
+    const bool have = xlogx != nullptr;  // exact mode has a table: block ranges and mantissa tables too
+    int64_t work = (have && table) ? n_rows + 1 : 0;
     if (work < m_pad) work = m_pad;
     int64_t tb = (work + 255) / 256;
     if (tb > (int64_t)num_sms * 16) tb = (int64_t)num_sms * 16;
-    unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, xlogx, n_rows, fix_s, blkrange,
-                                                         (xlogx && blkrange) ? (int)(m_pad / 128) : 0,
-                                                         xlogx ? fixr : nullptr);
+    unpack_prep_kernel<<<(unsigned)tb, 256, 0, stream>>>(colstat, m_pad, table ? xlogx : nullptr, n_rows, fix_s,
+                                                         blkrange, (have && blkrange) ? (int)(m_pad / 128) : 0,
+                                                         have ? fixr : nullptr);
     return cudaGetLastError();
 }
 

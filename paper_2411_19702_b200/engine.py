@@ -93,6 +93,7 @@ class Prepared:
     inv: torch.Tensor | None = None   # order "colsum": int32 column -> slot
     words: torch.Tensor | None = None  # word-operand path: the (m, nw) words the GEMM expands itself
     layout_knobs: tuple = ()  # ("fp4", "cta_group") at prepare time: X's format depends on them
+    stats_ready: bool = True  # False: the word-operand path's first compute() also computes the statistics
 
     def __post_init__(self):
         if not self.layout_knobs:
@@ -310,12 +311,11 @@ class MIEngine:
             raise DomainError("order='colsum' is single-GPU only (each rank would unpermute the whole matrix)")
         ld, m_pad = self.layout(n_rows, n_cols)
         if order == "natural" and self.words_operand(n_rows, n_cols):
-            # word-operand path: column statistics only; compute() expands the words in the GEMM
+            # word-operand path: nothing to expand; the first compute() also
+            # computes the column statistics (mi_gram_mi_words_stats: inside the
+            # fused launch for the full tile list of a narrow matrix)
             x, colsum, colstat = self._alloc_prepared(n_rows, n_cols, True)
-            nat.check(nat.lib().mi_colstat_words(words_dev.data_ptr(), n_rows, n_cols, colstat.data_ptr(),
-                                                 colsum.data_ptr(), _stream_ptr(self.device)),
-                      "mi_colstat_words")
-            return Prepared(n_rows, n_cols, ld, m_pad, None, colsum, colstat, words=words_dev)
+            return Prepared(n_rows, n_cols, ld, m_pad, None, colsum, colstat, words=words_dev, stats_ready=False)
         x, colsum, colstat = self._alloc_prepared(n_rows, n_cols)
         mask = self._rank_mask(n_cols, rank, world)
         if order == "colsum":
@@ -385,10 +385,18 @@ class MIEngine:
         if prep.x is None:
             if prep.words is None:
                 raise DomainError("word-operand prepare without words (prepare_range was not called)")
-            nat.check(nat.lib().mi_gram_mi_words(prep.words.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m,
-                                                 mode, eps, diag, kind, out.data_ptr(), ld_out,
-                                                 tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),
-                      "mi_gram_mi_words")
+            if prep.stats_ready:
+                nat.check(nat.lib().mi_gram_mi_words(prep.words.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m,
+                                                     mode, eps, diag, kind, out.data_ptr(), ld_out,
+                                                     tiles.data_ptr(), tiles.shape[0], _stream_ptr(self.device)),
+                          "mi_gram_mi_words")
+            else:
+                nat.check(nat.lib().mi_gram_mi_words_stats(prep.words.data_ptr(), prep.colstat.data_ptr(),
+                                                           prep.colsum.data_ptr(), prep.n_rows, m, mode, eps, diag,
+                                                           kind, out.data_ptr(), ld_out, tiles.data_ptr(),
+                                                           tiles.shape[0], _stream_ptr(self.device)),
+                          "mi_gram_mi_words_stats")
+                prep.stats_ready = True
             return out
         nat.check(nat.lib().mi_gram_mi(prep.x.data_ptr(), prep.colstat.data_ptr(), prep.n_rows, m, prep.ld,
                                        mode, eps, diag, kind, out.data_ptr(), ld_out,

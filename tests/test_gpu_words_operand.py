@@ -186,3 +186,47 @@ def test_layout_knob_change_between_prepare_and_compute_is_rejected(engine):
         with pytest.raises(DomainError):
             engine.compute(prep, None, torch.float64)
     engine.compute(prep, None, torch.float64)  # unchanged knobs: fine
+
+
+@pytest.mark.parametrize("n,m", [(300_000, 512), (2_000_000, 1000), (70_016, 700), (1_000_000, 256)])
+def test_statistics_inside_the_fused_launch(engine, n, m):
+    """xp_stats = 1: for the full tile list of a narrow matrix the column
+    statistics are computed inside the fused launch (the expanders count the
+    diagonal units' columns, the epilogue warps build the statistics behind
+    grid-wide barriers); every output equals the separate counting pass's."""
+    rng = np.random.default_rng(n + 3 * m)
+    dens = rng.uniform(0.02, 0.98, size=m)
+    bits = (rng.random((n, m)) < dens[None, :]).astype(np.uint8)
+    bits[:, 0] = 0
+    bits[:, 1] = 1
+    words = O.pack_bits(bits)
+    w = engine.upload(words)
+    cases = [(None, torch.float64), (None, torch.float32), (None, torch.int32),
+             (cfg_of("epsilon", 1e-9, False), torch.float64)]
+    res = {}
+    for xs in (1, 0):
+        with knobs(xp=1, xp_stats=xs):
+            outs = []
+            for cfg, dt in cases:
+                prep = engine.prepare(w, n, m)  # fresh: the first compute computes the statistics
+                outs.append(engine.compute(prep, cfg, dt).cpu().numpy())
+                outs.append(prep.colsum[:m].cpu().numpy())
+            res[xs] = outs
+    for a, b in zip(res[1], res[0]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(res[1][1].astype(np.uint64), bits.sum(axis=0).astype(np.uint64))
+
+
+def test_host_paths_with_fused_statistics(engine):
+    from paper_2411_19702_b200 import BinaryMatrix, gram_ones, mi_all_pairs
+
+    n, m = 400_000, 600
+    rng = np.random.default_rng(77)
+    words = O.pack_bits(rand_bits(rng, n, m, 0.35))
+    mat = BinaryMatrix(n, m, words)
+    res = {}
+    for xs in (1, 0):
+        with knobs(xp=1, xp_stats=xs, ingest=0):
+            res[xs] = [mi_all_pairs(mat).values, gram_ones(mat)]
+    for a, b in zip(res[1], res[0]):
+        assert np.array_equal(a, b)
