@@ -55,10 +55,13 @@ def _bytes(v, unit):
 
 
 def launches(path, out):
+    """Per-kernel launch counts, mean / total duration and share; with extra
+    --metrics (e.g. dram__bytes_read.sum), their per-launch means too."""
     rows = list(csv.reader(open(path)))
     hdr = None
-    agg = defaultdict(list)
-    order = []
+    time = defaultdict(list)
+    extra = defaultdict(lambda: defaultdict(list))
+    order, metrics = [], []
     for r in rows:
         if "Kernel Name" in r:
             hdr = r
@@ -67,18 +70,28 @@ def launches(path, out):
             d = dict(zip(hdr, r))
             name = d["Kernel Name"].split("(")[0][:90]
             val = float(d["Metric Value"].replace(",", ""))
-            scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1, "msecond": 1}.get(
-                d["Metric Unit"], 1e-6)
-            if name not in agg:
+            if name not in time and name not in extra:
                 order.append(name)
-            agg[name].append(val * scale)
-    total = sum(sum(v) for v in agg.values())
+            if d["Metric Name"] == "gpu__time_duration.sum":
+                scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1, "msecond": 1}.get(
+                    d["Metric Unit"], 1e-6)
+                time[name].append(val * scale)
+            else:
+                key = f"{d['Metric Name']} ({d['Metric Unit']})"
+                if key not in metrics:
+                    metrics.append(key)
+                extra[name][key].append(val)
+    total = sum(sum(v) for v in time.values())
     lines = [f"# launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`): `{path}`", "",
              "cold-cache, serialised per launch: compare SHARES, not absolutes.", "",
-             "| kernel | launches | mean ms | total ms | share |", "|---|---|---|---|---|"]
+             "| kernel | launches | mean ms | total ms | share |" + "".join(f" mean {k} |" for k in metrics),
+             "|---|---|---|---|---|" + "---|" * len(metrics)]
     for n in order:
-        v = agg[n]
-        lines.append(f"| {n} | {len(v)} | {sum(v)/len(v):.4f} | {sum(v):.3f} | {sum(v)/total*100:.1f}% |")
+        v = time.get(n, [])
+        if not v:
+            continue
+        ex = "".join(f" {sum(extra[n][k]) / len(extra[n][k]):.4g} |" if extra[n][k] else " - |" for k in metrics)
+        lines.append(f"| {n} | {len(v)} | {sum(v)/len(v):.4f} | {sum(v):.3f} | {sum(v)/total*100:.1f}% |" + ex)
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
