@@ -203,6 +203,14 @@ int mi_generate_words(uint64_t* d_words, int64_t n_rows, int64_t n_cols, uint64_
  * or float32 (MI_OUT_F32). */
 int mi_all_pairs_host(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,
                       double epsilon, int include_diagonal, int out_kind, void* h_out, int device);
+/* mi_all_pairs_host on several GPUs of this process (devices[0..n_devices)):
+ * the tiles are dealt as over the ranks of the multi-GPU path, every device
+ * uploads the words over its own link, computes its share and writes its tiles
+ * and mirrors straight into the host matrix over its own link (zero copy into
+ * h_out when it is pinned and mapped -- mi_host_register -- else into a cached
+ * pinned matrix copied out at the end).  Bit-identical to one device. */
+int mi_all_pairs_host_devices(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                              int include_diagonal, int out_kind, void* h_out, const int* devices, int n_devices);
 /* the same result as the packed upper triangle (MI_PACKED_UPPER layout,
  * n_cols (n_cols+1)/2 elements in h_out): half the device-to-host bytes */
 int mi_all_pairs_host_packed(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode,

@@ -18,6 +18,8 @@ from .engine import (
     gram_ones,
     mi_all_pairs,
     mi_all_pairs_c_abi,
+    mi_all_pairs_devices,
+    unpack_upper,
 )
 from .errors import (
     ConsistencyError,
@@ -33,6 +35,6 @@ __version__ = "0.1.0"
 __all__ = [
     "BinaryMatrix", "from_bits", "from_rows", "pack_bits", "unpack_bits",
     "BACKENDS", "MODES", "EngineConfig", "MIEngine", "MIMatrix",
-    "column_sums", "gram_ones", "mi_all_pairs", "mi_all_pairs_c_abi",
+    "column_sums", "gram_ones", "mi_all_pairs", "mi_all_pairs_c_abi", "mi_all_pairs_devices", "unpack_upper",
     "ConsistencyError", "DimensionError", "DomainError", "FormatError", "MiMatrixError", "NativeError",
 ]

@@ -79,6 +79,7 @@ SIGNATURES = {
     "mi_generate_words": (_int, [_vp, _i64, _i64, _u64, _vp, _vp, _vp, _u64, _u64, _vp]),
     "mi_all_pairs_host": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
     "mi_all_pairs_host_packed": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _int]),
+    "mi_all_pairs_host_devices": (_int, [_vp, _i64, _i64, _int, _dbl, _int, _int, _vp, _vp, _int]),
     "mi_gram_ones_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_column_sums_host": (_int, [_vp, _i64, _i64, _vp, _int]),
     "mi_host_register": (_int, [_vp, _i64]),

@@ -16,6 +16,7 @@
 #include <mutex>
 #include <thread>
 #include <condition_variable>
+#include <string>
 #include <vector>
 
 #include "../../include/mimatrix_b200.h"
@@ -719,9 +720,160 @@ int mi_copy_tiles_to_host(const void* d_out, int64_t ld_out, int64_t n_cols, int
     return MI_OK;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- several devices, one process
+//
+// mi_all_pairs_host over a list of devices: the upper-triangle tiles are dealt
+// as over the ranks of the multi-GPU path (mi_tile_list / mi_rank_blocks for
+// rank r of world n), each device uploads the words over its own link, unpacks
+// only its column blocks (the word-operand build: counts only), computes its
+// tiles tile-major, and writes its tiles and mirrors straight into the mapped
+// host matrix (mi_scatter_tiles' zero-copy kernel) over its own link.  One host
+// thread per device.  A device may be listed twice (tests run [0, 0] on one GPU).
+namespace mib200 {
+namespace capi {
+
+constexpr int kMaxSlots = 16;
+Workspace g_ws_slot[kMaxSlots];
+std::mutex g_multi_mu;
+void* g_multi_stage = nullptr;  // pinned (portable) copy of pageable words
+size_t g_multi_stage_cap = 0;
+void* g_multi_egress = nullptr;  // pinned, mapped, portable matrix for a pageable output
+size_t g_multi_egress_cap = 0;
+
+int grow_pinned(void** p, size_t* cap, size_t need, unsigned flags) {
+    if (*cap >= need && *p) return MI_OK;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *cap = 0;
+    MI_CUDA(cudaHostAlloc(p, need, flags));
+    *cap = need;
+    return MI_OK;
+}
+
+int multi_slot(int slot, int device, const uint64_t* src_words, int64_t n_rows, int64_t n_cols, int world, int mode,
+               double eps, int include_diagonal, int out_kind, void* h_dst) {
+    MI_CUDA(cudaSetDevice(device));
+    DevInfo info;
+    int rc = query_device(device, &info);
+    if (rc) return rc;
+    Workspace& ws = g_ws_slot[slot];
+    if (ws.device != device) release(ws);
+    if (ws.device < 0) {
+        ws.device = device;
+        MI_CUDA(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+        MI_CUDA(cudaStreamCreateWithFlags(&ws.copy_stream, cudaStreamNonBlocking));
+    }
+    const int64_t T = tiles_per_side(n_cols);
+    const std::vector<int32_t> tiles = rank_tiles(T, slot, world, tile_band());
+    const int64_t k = (int64_t)tiles.size() / 2;
+    if (k == 0) return MI_OK;
+    const int64_t nw = (n_rows + 63) / 64, ld = mi_kmajor_ld(n_rows), m_pad = mi_kmajor_rows(n_cols);
+    const int ts = mi_tile_size();
+    const size_t esz = out_kind == MI_OUT_F64 ? 8 : 4;
+    const bool xp = words_operand(n_rows, n_cols);
+    if ((rc = ensure(&ws.words, &ws.words_cap, (size_t)(n_cols * nw * 8)))) return rc;
+    if (!xp && (rc = ensure(&ws.x, &ws.x_cap, (size_t)(m_pad * ld)))) return rc;
+    if ((rc = ensure(&ws.colsum, &ws.colsum_cap, (size_t)(m_pad * 4 + T)))) return rc;  // + the block mask
+    if ((rc = ensure(&ws.colstat, &ws.colstat_cap, (size_t)mi_colstat_bytes(n_rows, n_cols)))) return rc;
+    if ((rc = ensure(&ws.tiles, &ws.tiles_cap, tiles.size() * 4))) return rc;
+    if ((rc = ensure(&ws.out, &ws.out_cap, (size_t)k * ts * ts * esz))) return rc;
+    MI_CUDA(cudaMemcpyAsync(ws.words, src_words, (size_t)(n_cols * nw * 8), cudaMemcpyHostToDevice, ws.stream));
+    MI_CUDA(cudaMemcpyAsync(ws.tiles, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, ws.stream));
+    uint8_t* d_mask = nullptr;
+    if (!xp) {  // expand only this slot's column blocks
+        std::vector<uint8_t> mask((size_t)T, 0);
+        const int64_t got = mi_rank_blocks(n_cols, slot, world, mask.data(), T);
+        if (got < 0) return (int)-got;
+        d_mask = (uint8_t*)ws.colsum + m_pad * 4;
+        MI_CUDA(cudaMemcpyAsync(d_mask, mask.data(), (size_t)T, cudaMemcpyHostToDevice, ws.stream));
+    }
+    MI_CUDA(launch_unpack_colsum((const uint64_t*)ws.words, n_rows, n_cols, nw, xp ? nullptr : (int8_t*)ws.x, ld, m_pad,
+                                 (int32_t*)ws.colsum, (ColStat*)ws.colstat, xlogx_ptr(ws.colstat, n_rows, n_cols),
+                                 blkrange_ptr(ws.colstat, n_rows, n_cols), fixr_ptr(ws.colstat, n_rows, n_cols),
+                                 operand_fp4(n_rows), d_mask, ts, info.num_sms, ws.stream));
+    if ((rc = launch_fused(xp ? nullptr : (const int8_t*)ws.x, ws.colstat, n_rows, n_cols, ld, mode, eps,
+                           include_diagonal, out_kind, ws.out, MI_TILE_MAJOR, (const int32_t*)ws.tiles, k, nullptr,
+                           ws.stream, xp ? (const uint64_t*)ws.words : nullptr)))
+        return rc;
+    void* d_dst = nullptr;  // the mapped host matrix as this device sees it
+    MI_CUDA(cudaHostGetDevicePointer(&d_dst, h_dst, 0));
+    MI_CUDA(launch_scatter_tiles(ws.out, (const int32_t*)ws.tiles, k, ts, n_cols, (int)esz, d_dst, n_cols, true,
+                                 ws.stream));
+    MI_CUDA(cudaStreamSynchronize(ws.stream));
+    return MI_OK;
+}
+
+}  // namespace capi
+}  // namespace mib200
+
+extern "C" {
+
+int mi_all_pairs_host_devices(const uint64_t* h_words, int64_t n_rows, int64_t n_cols, int mode, double epsilon,
+                              int include_diagonal, int out_kind, void* h_out, const int* devices, int n_devices) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if ((rc = check_mode(mode, epsilon, out_kind))) return rc;
+    if (out_kind == MI_OUT_COUNTS) return fail(MI_ERR_DOMAIN, "use mi_gram_ones_host for counts");
+    if (!devices || n_devices < 1 || n_devices > kMaxSlots)
+        return fail(MI_ERR_DOMAIN, "devices must list 1..%d device indices", kMaxSlots);
+    if (n_devices == 1)
+        return mi_all_pairs_host(h_words, n_rows, n_cols, mode, epsilon, include_diagonal, out_kind, h_out, devices[0]);
+    if ((rc = check_padding(h_words, n_rows, n_cols))) return rc;
+    for (int r = 0; r < n_devices; ++r) {
+        DevInfo info;
+        if ((rc = query_device(devices[r], &info))) return rc;
+    }
+    std::lock_guard<std::mutex> lk(g_multi_mu);
+    const int64_t nw = (n_rows + 63) / 64;
+    const size_t words_bytes = (size_t)(n_cols * nw * 8);
+    const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * (out_kind == MI_OUT_F64 ? 8 : 4);
+    const int threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    // inputs every device can DMA from: the caller's pinned words, or a portable pinned copy
+    const uint64_t* src = h_words;
+    if (!host_is_pinned(h_words)) {
+        if ((rc = grow_pinned(&g_multi_stage, &g_multi_stage_cap, words_bytes, cudaHostAllocPortable))) return rc;
+        parallel_memcpy(g_multi_stage, h_words, words_bytes, threads);
+        src = (const uint64_t*)g_multi_stage;
+    }
+    // output every device can write: the caller's mapped pinned matrix, or a cached one copied out at the end
+    void* dst = h_out;
+    cudaPointerAttributes a;
+    const bool mapped = cudaPointerGetAttributes(&a, h_out) == cudaSuccess && a.type == cudaMemoryTypeHost &&
+                        a.devicePointer != nullptr;
+    cudaGetLastError();
+    if (!mapped) {
+        if ((rc = grow_pinned(&g_multi_egress, &g_multi_egress_cap, out_bytes,
+                              cudaHostAllocPortable | cudaHostAllocMapped)))
+            return rc;
+        dst = g_multi_egress;
+    }
+    std::vector<int> rcs((size_t)n_devices, MI_OK);
+    std::vector<std::string> msgs((size_t)n_devices);
+    std::vector<std::thread> pool;
+    for (int r = 0; r < n_devices; ++r)
+        pool.emplace_back([&, r] {
+            rcs[(size_t)r] = multi_slot(r, devices[r], src, n_rows, n_cols, n_devices, mode, epsilon,
+                                        include_diagonal, out_kind, dst);
+            if (rcs[(size_t)r]) msgs[(size_t)r] = mi_last_error();
+        });
+    for (auto& t : pool) t.join();
+    for (int r = 0; r < n_devices; ++r)
+        if (rcs[(size_t)r]) return fail(rcs[(size_t)r], "device %d: %s", devices[r], msgs[(size_t)r].c_str());
+    if (!mapped) parallel_memcpy(h_out, dst, out_bytes, threads);
+    return MI_OK;
+}
+
 void mi_release_workspace(void) {
-    std::lock_guard<std::mutex> lk(g_ws_mu);
-    for (auto& w : g_ws) release(w);
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        for (auto& w : g_ws) release(w);
+    }
+    std::lock_guard<std::mutex> lk(g_multi_mu);
+    for (auto& w : g_ws_slot) release(w);
+    if (g_multi_stage) cudaFreeHost(g_multi_stage), g_multi_stage = nullptr, g_multi_stage_cap = 0;
+    if (g_multi_egress) cudaFreeHost(g_multi_egress), g_multi_egress = nullptr, g_multi_egress_cap = 0;
 }
 
 }  // extern "C"

@@ -526,21 +526,49 @@ class MIEngine:
 
 
 def mi_all_pairs(data, cfg: EngineConfig | None = None, backend: str = "dense", threads: int = 0,
-                 device: int | None = None) -> MIMatrix:
+                 device: int | None = None, devices=None) -> MIMatrix:
     """Full pairwise MI matrix (drop-in for engine.mi_all_pairs, engine.py:144-168).
 
     ``backend`` must be one of the reference's names ("dense", "sparse",
     "direct"); all run the same GPU path.  ``threads`` is accepted and ignored:
-    results are bit-identical regardless of parallelism.
+    results are bit-identical regardless of parallelism.  ``devices``: a list
+    of GPU indices to share the work in this process (mi_all_pairs_devices).
     """
     if backend not in BACKENDS:
         raise DomainError(f"backend must be one of {BACKENDS}, got {backend!r}")
     _config_fields(cfg)
+    if devices is not None and len(devices) > 1:
+        return MIMatrix(values=mi_all_pairs_devices(data, devices, cfg))
     n, m, words = as_dense_words(data)
-    eng = MIEngine.get(device)
+    eng = MIEngine.get(device if devices is None else devices[0])
     values = np.empty((m, m), dtype=np.float64)  # fresh, caller-owned, like the reference's
     eng.all_pairs_host(words, n, m, cfg, torch.float64, host_out=values)
     return MIMatrix(values=values)
+
+
+def mi_all_pairs_devices(data, devices, cfg: EngineConfig | None = None, out_dtype=np.float64,
+                         out: np.ndarray | None = None) -> np.ndarray:
+    """The full matrix from several GPUs of this process (C ABI
+    mi_all_pairs_host_devices): the triangle's tiles are dealt as over the
+    ranks of the multi-GPU path, each device uploads the words and writes its
+    tiles and mirrors into the host matrix over its own link (zero copy when
+    ``out`` is pinned and mapped, e.g. registered with mi_host_register).  A
+    device may be listed more than once (it then runs several shares)."""
+    mode, eps, diag = _config_fields(cfg)
+    n, m, words = as_dense_words(data)
+    devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+    if devs.ndim != 1 or devs.size < 1:
+        raise DomainError("devices must be a non-empty list of GPU indices")
+    if out is None:
+        out = np.empty((m, m), dtype=out_dtype)
+    if out.dtype not in (np.float64, np.float32) or out.shape != (m, m) or not out.flags.c_contiguous:
+        raise DimensionError(f"out must be a C-contiguous ({m}, {m}) float64 or float32 array")
+    kind = nat.MI_OUT_F64 if out.dtype == np.float64 else nat.MI_OUT_F32
+    w = np.ascontiguousarray(words)
+    nat.check(nat.lib().mi_all_pairs_host_devices(w.ctypes.data, n, m, mode, eps, diag, kind, out.ctypes.data,
+                                                  devs.ctypes.data, int(devs.size)),
+              "mi_all_pairs_host_devices")
+    return out
 
 
 def unpack_upper(packed, m: int):
