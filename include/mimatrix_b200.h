@@ -171,6 +171,14 @@ int mi_gram_mi_words_stats(const uint64_t* d_words, void* d_colstat, int32_t* d_
  * neither 0 nor 1 (from_rows's DomainError); the words are then not valid. */
 int mi_pack_bits(const uint8_t* d_bits, int64_t n_rows, int64_t n_cols, int64_t ld_bits, uint64_t* d_words,
                  int32_t* d_bad, void* stream);
+/* binmat.to_dense (binmat.py:187-194) on the device, for the sparse backend's
+ * SparseBinaryMatrix (per-column row-index lists, binmat.py:100-133): CSC
+ * arrays d_indptr[n_cols + 1] (int64 offsets into d_indices) and d_indices
+ * (int64 row indices) -> the words layout (zeroed, then the bits set; cost ~
+ * nnz).  *d_bad (device int32, zeroed by the caller) gets bit 0 set for an
+ * index outside [0, n_rows) (the words are then not valid). */
+int mi_pack_sparse(const int64_t* d_indices, const int64_t* d_indptr, int64_t n_rows, int64_t n_cols,
+                   uint64_t* d_words, int32_t* d_bad, void* stream);
 /* ---- column order by column sum (configs with spread densities) ----
  * The fused epilogue's FP64-free table path needs each tile's column sums to
  * be clustered; computing in slots ordered by column sum makes that true for

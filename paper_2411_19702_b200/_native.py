@@ -66,6 +66,7 @@ SIGNATURES = {
     "mi_unpack_colsum": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp]),
     "mi_unpack_colsum_blocks": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
     "mi_pack_bits": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "mi_pack_sparse": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "mi_unpack_prep": (_int, [_i64, _i64, _vp, _vp]),
     "mi_unpack_colsum_range": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _vp]),
     "mi_column_order": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),

@@ -334,6 +334,18 @@ int mi_pack_bits(const uint8_t* d_bits, int64_t n_rows, int64_t n_cols, int64_t 
     return MI_OK;
 }
 
+int mi_pack_sparse(const int64_t* d_indices, const int64_t* d_indptr, int64_t n_rows, int64_t n_cols,
+                   uint64_t* d_words, int32_t* d_bad, void* stream) {
+    int rc = check_shape(n_rows, n_cols);
+    if (rc) return rc;
+    if (!d_indptr || !d_words || !d_bad) return fail(MI_ERR_DOMAIN, "d_indptr, d_words and d_bad are required");
+    DevInfo info;
+    if ((rc = current_device_info(&info))) return rc;
+    MI_CUDA(launch_pack_sparse(d_indices, d_indptr, n_rows, n_cols, d_words, reinterpret_cast<int*>(d_bad),
+                               info.num_sms, (cudaStream_t)stream));
+    return MI_OK;
+}
+
 int mi_column_order(const uint64_t* d_words, int64_t n_rows, int64_t n_cols, int32_t* d_perm, int32_t* d_inv,
                     int32_t* d_spread, void* stream) {
     int rc = check_shape(n_rows, n_cols);

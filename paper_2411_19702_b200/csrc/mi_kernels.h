@@ -136,6 +136,11 @@ cudaError_t launch_unpack_range(const uint64_t* words, int64_t n_rows, int64_t m
 cudaError_t launch_pack_bits(const uint8_t* bits, int64_t n_rows, int64_t m, int64_t ld, uint64_t* words, int* bad,
                              cudaStream_t stream);
 
+// binmat.to_dense on the device (pack.cu): CSC row indices (indptr[m + 1]) ->
+// words (zeroed first); *bad |= 1 on an index outside [0, n_rows).
+cudaError_t launch_pack_sparse(const int64_t* indices, const int64_t* indptr, int64_t n_rows, int64_t m,
+                               uint64_t* words, int* bad, int num_sms, cudaStream_t stream);
+
 // Column order by column sum (order.cu): perm[s] = column in operand slot s
 // (ascending sum, ties by column index), inv[perm[s]] = s; spread (device
 // int[2], or nullptr) = (min, max) column sum.

@@ -90,4 +90,50 @@ cudaError_t launch_pack_bits(const uint8_t* bits, int64_t n_rows, int64_t m, int
     return cudaGetLastError();
 }
 
+// binmat.to_dense (binmat.py:187-194) for the sparse backend's data,
+// SparseBinaryMatrix (per-column sorted row-index lists, binmat.py:100-133):
+// the CSC index arrays -> the words layout, on the device, cost ~ nnz.  A warp
+// takes 32 consecutive indices of one column (sorted, so neighbours mostly share
+// a word): the lanes of each word (__match_any_sync) OR their bits together and
+// one of them does the atomicOr.  An index outside [0, n_rows) sets *bad.
+__global__ void __launch_bounds__(256) pack_sparse_kernel(const int64_t* __restrict__ indices,
+                                                          const int64_t* __restrict__ indptr, int64_t n_rows,
+                                                          int64_t m, int64_t nw, unsigned long long* __restrict__ words,
+                                                          int* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; c < m; c += warps) {
+        const int64_t b = indptr[c], e = indptr[c + 1];
+        for (int64_t i0 = b; i0 < e; i0 += 32) {
+            const int64_t i = i0 + lane;
+            const bool in = i < e;
+            int64_t r = in ? indices[i] : 0;
+            if (in && (r < 0 || r >= n_rows)) {
+                atomicOr(bad, 1);
+                r = 0;
+            }
+            const unsigned act = __ballot_sync(0xffffffffu, in);
+            const long long w = in ? r >> 6 : -1 - lane;  // idle lanes never match a word
+            const unsigned grp = __match_any_sync(0xffffffffu, w);
+            const unsigned long long bit = in ? 1ull << (r & 63) : 0ull;
+            // OR of the group's bits: 64-bit as two 32-bit reductions
+            const unsigned lo = __reduce_or_sync(grp, (unsigned)bit), hi = __reduce_or_sync(grp, (unsigned)(bit >> 32));
+            if (in && lane == __ffs(grp & act) - 1)
+                atomicOr(words + c * nw + w, ((unsigned long long)hi << 32) | lo);
+        }
+    }
+}
+
+cudaError_t launch_pack_sparse(const int64_t* indices, const int64_t* indptr, int64_t n_rows, int64_t m,
+                               uint64_t* words, int* bad, int num_sms, cudaStream_t stream) {
+    const int64_t nw = (n_rows + 63) / 64;
+    cudaError_t e = cudaMemsetAsync(words, 0, (size_t)(m * nw * 8), stream);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (m + 7) / 8;
+    if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+    pack_sparse_kernel<<<(unsigned)blocks, 256, 0, stream>>>(indices, indptr, n_rows, m, nw,
+                                                             reinterpret_cast<unsigned long long*>(words), bad);
+    return cudaGetLastError();
+}
+
 }  // namespace mib200

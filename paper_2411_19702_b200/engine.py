@@ -203,6 +203,31 @@ class MIEngine:
         words = self.pack_bits(host.to(self.device, non_blocking=False))
         return BinaryMatrix(int(arr.shape[0]), int(arr.shape[1]), words.cpu().numpy().view(np.uint64))
 
+    def from_sparse(self, sparse) -> torch.Tensor:
+        """binmat.to_dense (binmat.py:187-194) on the device for the sparse
+        backend's data (a SparseBinaryMatrix: per-column sorted row-index
+        lists): upload the CSC index arrays, set the bits (mi_pack_sparse; cost
+        ~ nnz, no N x m host matrix).  Returns device words (m, nw)."""
+        n, m = int(sparse.n_rows), int(sparse.n_cols)
+        if n < 1 or m < 1:
+            raise DimensionError("matrix must have at least one row and one column")
+        cols = [np.asarray(ix, dtype=np.int64).ravel() for ix in sparse.col_indices]
+        if len(cols) != m:
+            raise DimensionError("col_indices must hold one list per column")
+        indptr = np.zeros(m + 1, dtype=np.int64)
+        np.cumsum([c.size for c in cols], out=indptr[1:])
+        idx = np.concatenate(cols) if indptr[-1] else np.zeros(1, dtype=np.int64)
+        d_idx = torch.from_numpy(idx).to(self.device)
+        d_ptr = torch.from_numpy(indptr).to(self.device)
+        words = torch.empty((m, n_words(n)), dtype=torch.int64, device=self.device)
+        bad = torch.zeros((1,), dtype=torch.int32, device=self.device)
+        nat.check(nat.lib().mi_pack_sparse(d_idx.data_ptr(), d_ptr.data_ptr(), n, m, words.data_ptr(),
+                                           bad.data_ptr(), _stream_ptr(self.device)),
+                  "mi_pack_sparse")
+        if int(bad.item()) != 0:
+            raise DomainError(f"row index out of range [0, {n})")
+        return words
+
     def upload(self, words: np.ndarray) -> torch.Tensor:
         """Host words (m, nw) uint64 -> device tensor (int64 storage, same bits)."""
         host = torch.from_numpy(np.ascontiguousarray(words).view(np.int64))
@@ -525,6 +550,15 @@ class MIEngine:
         return host_out
 
 
+def _host_words(data, device: int | None = None) -> tuple[int, int, np.ndarray]:
+    """(n_rows, n_cols, words) of any input: dense words as they are; the
+    sparse backend's index lists packed on the GPU (MIEngine.from_sparse)."""
+    if not hasattr(data, "words") and hasattr(data, "col_indices"):
+        w = MIEngine.get(device).from_sparse(data)
+        return int(data.n_rows), int(data.n_cols), w.cpu().numpy().view(np.uint64)
+    return as_dense_words(data)
+
+
 def mi_all_pairs(data, cfg: EngineConfig | None = None, backend: str = "dense", threads: int = 0,
                  device: int | None = None, devices=None) -> MIMatrix:
     """Full pairwise MI matrix (drop-in for engine.mi_all_pairs, engine.py:144-168).
@@ -539,7 +573,7 @@ def mi_all_pairs(data, cfg: EngineConfig | None = None, backend: str = "dense", 
     _config_fields(cfg)
     if devices is not None and len(devices) > 1:
         return MIMatrix(values=mi_all_pairs_devices(data, devices, cfg))
-    n, m, words = as_dense_words(data)
+    n, m, words = _host_words(data, device if devices is None else devices[0])
     eng = MIEngine.get(device if devices is None else devices[0])
     values = np.empty((m, m), dtype=np.float64)  # fresh, caller-owned, like the reference's
     eng.all_pairs_host(words, n, m, cfg, torch.float64, host_out=values)
@@ -555,7 +589,7 @@ def mi_all_pairs_devices(data, devices, cfg: EngineConfig | None = None, out_dty
     ``out`` is pinned and mapped, e.g. registered with mi_host_register).  A
     device may be listed more than once (it then runs several shares)."""
     mode, eps, diag = _config_fields(cfg)
-    n, m, words = as_dense_words(data)
+    n, m, words = _host_words(data, int(list(devices)[0]) if len(list(devices)) else None)
     devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
     if devs.ndim != 1 or devs.size < 1:
         raise DomainError("devices must be a non-empty list of GPU indices")
@@ -590,7 +624,7 @@ def unpack_upper(packed, m: int):
 
 def gram_ones(data, device: int | None = None) -> np.ndarray:
     """Drop-in for gram.gram_ones (gram.py:56-65): int64 m x m co-occurring ones."""
-    n, m, words = as_dense_words(data)
+    n, m, words = _host_words(data, device)
     out = np.empty((m, m), dtype=np.int64)
     w = np.ascontiguousarray(words)
     dev = MIEngine.get(device).device.index
@@ -600,7 +634,7 @@ def gram_ones(data, device: int | None = None) -> np.ndarray:
 
 def column_sums(data, device: int | None = None) -> np.ndarray:
     """Drop-in for binmat.column_sums (binmat.py:175-177), computed by kernel 1."""
-    n, m, words = as_dense_words(data)
+    n, m, words = _host_words(data, device)
     out = np.empty((m,), dtype=np.uint64)
     w = np.ascontiguousarray(words)
     dev = MIEngine.get(device).device.index
@@ -614,7 +648,7 @@ def mi_all_pairs_c_abi(data, cfg: EngineConfig | None = None, device: int = 0,
     """Same computation through the pure C entry point mi_all_pairs_host (what a
     non-Python binding would call); used by tests and the e2e cross-check."""
     mode, eps, diag = _config_fields(cfg)
-    n, m, words = as_dense_words(data)
+    n, m, words = _host_words(data, device)
     out = np.empty((m, m), dtype=out_dtype)
     kind = nat.MI_OUT_F64 if out_dtype == np.float64 else nat.MI_OUT_F32
     w = np.ascontiguousarray(words)

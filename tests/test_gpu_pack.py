@@ -80,3 +80,42 @@ def test_engine_from_bits_host(engine):
     bad8[10, 20] = 2
     with pytest.raises(DomainError):
         engine.from_bits(bad8)
+
+
+class _Sparse:
+    """The reference's SparseBinaryMatrix shape (binmat.py:100-133): per-column
+    sorted row-index lists."""
+
+    def __init__(self, n, m, cols):
+        self.n_rows, self.n_cols, self.col_indices = n, m, tuple(cols)
+
+
+def _sparse_of(bits):
+    return _Sparse(bits.shape[0], bits.shape[1], [np.flatnonzero(bits[:, j]).astype(np.int64)
+                                                  for j in range(bits.shape[1])])
+
+
+@pytest.mark.parametrize("n,m,d", [(1, 1, 1.0), (63, 3, 0.5), (65, 40, 0.3), (1000, 257, 0.01), (20_000, 600, 0.002),
+                                   (4096, 33, 0.0), (777, 129, 1.0)])
+def test_pack_sparse_matches_dense(engine, n, m, d):
+    """binmat.to_dense on the device: the index lists give the same words as
+    packing the dense matrix, and the drop-in / gram_ones / column_sums on
+    sparse input equal the dense results."""
+    from paper_2411_19702_b200 import BinaryMatrix, column_sums, gram_ones, mi_all_pairs
+
+    rng = np.random.default_rng(n * 31 + m)
+    bits = (rng.random((n, m)) < d).astype(np.uint8)
+    sp = _sparse_of(bits)
+    words = engine.from_sparse(sp).cpu().numpy().view(np.uint64)
+    assert np.array_equal(words, O.pack_bits(bits))
+    dense = BinaryMatrix(n, m, O.pack_bits(bits))
+    assert np.array_equal(mi_all_pairs(sp, backend="sparse").values, mi_all_pairs(dense).values)
+    assert np.array_equal(gram_ones(sp), gram_ones(dense))
+    assert np.array_equal(column_sums(sp), column_sums(dense))
+
+
+def test_pack_sparse_rejects_out_of_range(engine):
+    from paper_2411_19702_b200 import DomainError
+
+    with pytest.raises(DomainError):
+        engine.from_sparse(_Sparse(10, 2, [np.array([0, 3]), np.array([10])]))
