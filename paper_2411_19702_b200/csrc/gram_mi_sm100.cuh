@@ -864,11 +864,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         //   words), so it costs a shared-memory drain, not a DRAM latency.
         // The pacer slot idles.  Diagonal tiles stage one copy (B = A).
         if constexpr (XP) {
-            const bool spin = (p.debug & 256) != 0;  // experiments: spin instead of suspend-hinted waits
-            auto xwait = [&](uint32_t bar, uint32_t par) {
-                if (spin) mbar_wait_spin(bar, par);
-                else mbar_wait(bar, par);
-            };
+            auto xwait = [&](uint32_t bar, uint32_t par) { mbar_wait(bar, par); };
             // experiments: per-phase cycle sums of cluster 0 (tools/xp_probe.py --trace)
             long long* const xtr = (p.trace && cluster == 0) ? p.trace + 2048 : nullptr;
             const uint32_t raw0 = base + L::raw_off;

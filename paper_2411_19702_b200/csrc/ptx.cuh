@@ -116,33 +116,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
-// The same wait with cluster-scope acquire: the barrier's arrivals include
-// remote arrives (release.cluster) of the peer CTA's producer threads.
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-    const long long t0 = clock64();
-    while (!mbar_try_wait_cluster(bar, parity)) {
-        if (clock64() - t0 > (long long)20000000000LL) __trap();
-    }
-}
-
-// Spin on try_wait without a suspend hint (short waits on a hot pipeline).
-__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
-    const long long t0 = clock64();
-    while (!mbar_try_wait(bar, parity)) {
-        if (clock64() - t0 > (long long)20000000000LL) __trap();
-    }
-}
+// Relaxed arrive on a barrier that may live in another CTA of the cluster: the
+// caller has already made its writes visible (the word-operand expanders'
+// proxy fence drains their shared-memory stores), so no GPU-wide drain here.
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
