@@ -57,5 +57,5 @@ for cfg in [int(x) for x in a.configs.split(",")]:
         print(json.dumps({"cfg": cfg, "world": world, "rank_ms": [round(t, 3) for t in ts], "tiles": tiles,
                           "max_ms": round(max(ts), 3), "compute_efficiency": round(t1 / (world * max(ts)), 3)}),
               flush=True)
-    del out, w
+    del bufs, w
     torch.cuda.empty_cache()
