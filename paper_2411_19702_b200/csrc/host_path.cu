@@ -103,6 +103,15 @@ bool host_is_pinned(const void* h) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
+// Host threads copying between pageable user memory and pinned buffers: one
+// per core up to 16 (MI_B200_COPY_THREADS overrides).  A fresh output's first
+// touch (page faults) rides on these copies: config 3's drop-in takes 45.5 ms
+// with 8 threads and 38.4 ms with 16 on the 16-core host (tools/dropin_e2e.py).
+int copy_threads_default() {
+    const int hw = (int)std::thread::hardware_concurrency();
+    return std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", hw > 0 ? hw : 8)));
+}
+
 // Host copy threads between pageable user memory and the pinned staging
 // buffers: one thread reaches ~10 GB/s, well short of the link's ~55.  The
 // workers are a small persistent pool (created on first use, never torn
@@ -197,7 +206,7 @@ int upload_words(Workspace& ws, const uint64_t* h_words, int64_t n_cols, int64_t
         MI_CUDA(cudaHostAlloc(&ws.h_stage, bytes, cudaHostAllocDefault));
         ws.h_stage_cap = bytes;
     }
-    const int threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    const int threads = copy_threads_default();
     const int64_t chunks = n_cols >= 4 ? 4 : 1;
     for (int64_t k = 0; k < chunks; ++k) {
         const int64_t c0 = n_cols * k / chunks, c1 = n_cols * (k + 1) / chunks;
@@ -385,7 +394,7 @@ int all_pairs_host_staged(Workspace& ws, const uint64_t* h_words, int64_t n_rows
         }
         src_words = (const uint64_t*)ws.h_stage;
     }
-    const int copy_threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    const int copy_threads = copy_threads_default();
     // pageable output: D2H into the pinned egress buffer, pieces copied out below
     const bool stage_out = !host_is_pinned(h_out);
     char* d2h_dst = (char*)h_out;
@@ -611,7 +620,7 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
     MI_CUDA(cudaStreamSynchronize(ws->copy_stream));
     MI_CUDA(cudaStreamSynchronize(ws->stream));
     if (stage_out)
-        parallel_memcpy(h_out, d2h_dst, row_off(n_cols), std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8))));
+        parallel_memcpy(h_out, d2h_dst, row_off(n_cols), copy_threads_default());
     stamp("done");
     return MI_OK;
 }
@@ -829,7 +838,7 @@ int mi_all_pairs_host_devices(const uint64_t* h_words, int64_t n_rows, int64_t n
     const int64_t nw = (n_rows + 63) / 64;
     const size_t words_bytes = (size_t)(n_cols * nw * 8);
     const size_t out_bytes = (size_t)n_cols * (size_t)n_cols * (out_kind == MI_OUT_F64 ? 8 : 4);
-    const int threads = std::max(1, std::min(16, env_int("MI_B200_COPY_THREADS", 8)));
+    const int threads = copy_threads_default();
     // inputs every device can DMA from: the caller's pinned words, or a portable pinned copy
     const uint64_t* src = h_words;
     if (!host_is_pinned(h_words)) {
