@@ -32,8 +32,10 @@ struct GramMiParams {
     int l2_hint;            // 0 normal, 1 evict_last, 2 evict_first for operand loads
     int debug;              // experiments only (bit mask): 1 = compute but skip the output stores,
                             // 2 = skip the mirror stores, 4 = skip the direct stores, 8 = L2
-                            // evict_first hint on the output stores, 16 = no MMAs (data movement only)
-    long long* trace;       // experiments only: per-tile timestamps of cluster 0 (or nullptr)
+                            // evict_first hint on the output stores, 16 = no MMAs (data movement only);
+                            // word-operand build: 32 = no expansion, 64 = no word loads
+    long long* trace;       // experiments only: per-tile timestamps of cluster 0 (or nullptr); word-operand
+                            // build: per-phase cycle sums of cluster 0's expanders at [2048, 2080)
     unsigned long long rcp; // fixed point: round(2^(62 + nb) / N), nb = bit length of N
     int off0;               // fixed point: -(nb - 2) - s
     int fix_s;              // fixed point: scale s of the c log2 c terms
