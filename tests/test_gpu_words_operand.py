@@ -62,6 +62,10 @@ SHAPES = [
     (1, 1, 1.0), (300, 5, 0.5), (1000, 257, 0.3), (4099, 511, 0.5), (4200, 511, 0.5), (20_000, 700, 0.1),
     (129, 1, 0.5), (1_000_000, 100, 0.5),
     (70_001, 513, 0.45), (250_000, 256, 0.5), (600_000, 300, 0.02), (64 * 4 * 77 + 64, 600, 0.7),
+    # even word counts (the word-operand build runs): tiny m, m below one
+    # 128-row half, ragged K tails, tall N
+    (128, 1, 0.5), (1024, 5, 0.7), (8192, 100, 0.2), (6400, 130, 0.5), (65_536 + 128, 255, 0.4),
+    (1_000_064, 64, 0.5), (300_032, 1023, 0.05),
 ]
 
 
@@ -104,7 +108,7 @@ def test_tail_schedules(engine, tail, n, m):
 def test_output_forms_and_tile_subsets(engine):
     from paper_2411_19702_b200.engine import unpack_upper
 
-    n, m = 90_000, 1000
+    n, m = 90_112, 1000  # an even word count: the word-operand build runs
     rng = np.random.default_rng(17)
     words = O.pack_bits(rand_bits(rng, n, m, 0.25))
 
