@@ -290,7 +290,8 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * "f32_epi" (float32 output, exact mode: tiles off the table path run the
  * FP32-pipe epilogue beside the next tile's MMAs; 1 default, 0 = FP64), "xp"
  * (the word-operand build of mi_all_pairs_host and the Python engine: -1 auto
- * = when m_pad <= "xp_cols", default 3072; 0 never; 1 whenever the operands
+ * = when m_pad <= "xp_cols", default 3072 (a third of it for an odd word count
+ * per column, which needs a padded copy); 0 never; 1 whenever the operands
  * are e2m1).  Also settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */

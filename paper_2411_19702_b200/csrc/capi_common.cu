@@ -76,12 +76,17 @@ bool operand_fp4(int64_t n_rows) { return tuning().fp4 && tuning().cta_group == 
 // The word-operand build (expansion inside the GEMM's producer, no X in HBM)
 // where writing and re-reading X costs a large share of the step: narrow m
 // (the unpack is O(N m), the GEMM O(N m^2)).  Knob "xp": -1 auto (m_pad <=
-// "xp_cols"), 0 never, 1 whenever the operands are e2m1.
+// "xp_cols", a third of it for odd word counts), 0 never, 1 whenever the
+// operands are e2m1.
 bool words_operand(int64_t n_rows, int64_t n_cols) {
     const Tuning& t = tuning();
-    // (the words' TMA map needs a row pitch of a multiple of 16 bytes: nw even)
-    if (!operand_fp4(n_rows) || t.xp == 0 || ((n_rows + 63) / 64) % 2 != 0) return false;
-    return t.xp == 1 || round_up(n_cols < 1 ? 1 : n_cols, 256) <= t.xp_cols;
+    if (!operand_fp4(n_rows) || t.xp == 0) return false;
+    // an odd word count per column costs the build a padded copy of the words
+    // (its TMA map needs a 16-byte row pitch): N = 8e6 + 64, m = 512 steps
+    // 0.87 ms against 0.52 ms with an even count and 0.94 ms on the unpack
+    // path; at m = 2048 the two paths tie.  So the limit is a third of xp_cols.
+    const bool odd = ((n_rows + 63) / 64) % 2 != 0;
+    return t.xp == 1 || round_up(n_cols < 1 ? 1 : n_cols, 256) <= (odd ? t.xp_cols / 3 : t.xp_cols);
 }
 int prefetch_dist() { return tuning().prefetch; }
 int l2_hint() { return tuning().l2_hint; }

@@ -165,13 +165,14 @@ int make_tmap(CUtensorMap* tm, const int8_t* x, int64_t ld, int64_t m_pad) {
 
 // The packed words (m, nw) uint64 as a 2-D TMA tensor for the word-operand
 // build: 16-word (4 k-block, 128-byte) x 128-column boxes, 128-byte swizzle,
-// zero fill beyond nw and m.  The row pitch nw * 8 must be a multiple of 16.
-int make_tmap_words(CUtensorMap* tm, const uint64_t* words, int64_t nw, int64_t m) {
+// zero fill beyond nw and m.  The row pitch (words) must be even: a multiple
+// of 16 bytes.
+int make_tmap_words(CUtensorMap* tm, const uint64_t* words, int64_t nw, int64_t pitch, int64_t m) {
     PFN_cuTensorMapEncodeTiled_v12000 enc;
     int rc = get_encode(&enc);
     if (rc) return rc;
     cuuint64_t gdim[2] = {(cuuint64_t)nw, (cuuint64_t)m};
-    cuuint64_t gstride[1] = {(cuuint64_t)nw * 8};
+    cuuint64_t gstride[1] = {(cuuint64_t)pitch * 8};
     cuuint32_t box[2] = {16, 128};
     cuuint32_t estride[2] = {1, 1};
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(words), gdim, gstride, box, estride,
@@ -437,15 +438,45 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     if (n_tiles == 0) return MI_OK;
     if (out_kind == MI_OUT_COUNTS && mode != MI_MODE_EXACT)
         return fail(MI_ERR_DOMAIN, "counts export ignores the mode; pass MI_MODE_EXACT");
-    if (xp && ((reinterpret_cast<uintptr_t>(d_words) & 15) != 0 || ((n_rows + 63) / 64) % 2 != 0))
-        return fail(MI_ERR_DOMAIN, "the word-operand build needs 16-byte aligned words and an even word count per column");
+    if (xp && (reinterpret_cast<uintptr_t>(d_words) & 7) != 0) return fail(MI_ERR_DOMAIN, "words must be 8-byte aligned");
     if (!xp && (reinterpret_cast<uintptr_t>(d_kmajor) & 15) != 0)
         return fail(MI_ERR_DOMAIN, "kmajor operand must be 16-byte aligned");
     DevInfo info;
     if ((rc = current_device_info(&info))) return rc;
     CUtensorMap tm;
     if (!xp && (rc = make_tmap(&tm, d_kmajor, ld, mi_kmajor_rows(n_cols)))) return rc;
-    if (xp && (rc = make_tmap_words(&tm, d_words, (n_rows + 63) / 64, n_cols))) return rc;
+    // The words' TMA map needs a row pitch of a multiple of 16 bytes: an odd word
+    // count per column (or a misaligned base) is first copied with one pad word
+    // per column (stream-ordered scratch kept in the pool between calls; 0.5 GB
+    // at N = 8e6, m = 512)
+    const int64_t nw_x = (n_rows + 63) / 64;
+    uint64_t* padded = nullptr;
+    struct AsyncFree {  // released on the stream after whatever this call enqueued
+        void** p;
+        cudaStream_t s;
+        ~AsyncFree() {
+            if (*p) cudaFreeAsync(*p, s);
+        }
+    } padded_guard{(void**)&padded, stream};
+    if (xp && ((nw_x & 1) || (reinterpret_cast<uintptr_t>(d_words) & 15))) {
+        const int64_t pitch = nw_x + (nw_x & 1);
+        const size_t bytes = (size_t)(n_cols * pitch * 8);
+        cudaMemPool_t pool;
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
+            uint64_t keep = 0;
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            if (keep < bytes) {
+                keep = bytes;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
+        MI_CUDA(cudaMallocAsync((void**)&padded, bytes, stream));
+        MI_CUDA(launch_pitch_words(d_words, nw_x, padded, pitch, n_cols, info.num_sms, stream));
+        if ((rc = make_tmap_words(&tm, padded, nw_x, pitch, n_cols))) return rc;
+    } else if (xp && (rc = make_tmap_words(&tm, d_words, nw_x, nw_x, n_cols))) {
+        return rc;
+    }
     GramMiParams p;
     p.words = d_words;
     p.nw = (n_rows + 63) / 64;

@@ -143,6 +143,10 @@ cudaError_t launch_pack_bits(const uint8_t* bits, int64_t n_rows, int64_t m, int
 cudaError_t launch_pack_sparse(const int64_t* indices, const int64_t* indptr, int64_t n_rows, int64_t m,
                                uint64_t* words, int* bad, int num_sms, cudaStream_t stream);
 
+// words (m, nw) -> the same with row pitch `pitch` words (pack.cu)
+cudaError_t launch_pitch_words(const uint64_t* src, int64_t nw, uint64_t* dst, int64_t pitch, int64_t m, int num_sms,
+                               cudaStream_t stream);
+
 // Column order by column sum (order.cu): perm[s] = column in operand slot s
 // (ascending sum, ties by column index), inv[perm[s]] = s; spread (device
 // int[2], or nullptr) = (min, max) column sum.

@@ -136,4 +136,34 @@ cudaError_t launch_pack_sparse(const int64_t* indices, const int64_t* indptr, in
     return cudaGetLastError();
 }
 
+// The words with a row pitch of `pitch` >= nw words (the word-operand build's
+// TMA map needs a 16-byte multiple): one warp per column row and pass, 32
+// consecutive words per load; the pad words are not written (TMA never reads
+// them: its map's extent is nw).
+__global__ void __launch_bounds__(256) pitch_words_kernel(const unsigned long long* __restrict__ src, int64_t nw,
+                                                          unsigned long long* __restrict__ dst, int64_t pitch,
+                                                          int64_t m) {
+    // block (x, y): words [x * 2048, +2048) of columns y, y + gridDim.y, ...; 8 loads in flight per thread
+    const int64_t w0 = (int64_t)blockIdx.x * 2048 + threadIdx.x;
+    for (int64_t c = blockIdx.y; c < m; c += gridDim.y) {
+        const unsigned long long* s = src + c * nw;
+        unsigned long long* d = dst + c * pitch;
+        unsigned long long v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = w0 + 256 * k < nw ? __ldcs(s + w0 + 256 * k) : 0ull;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (w0 + 256 * k < nw) d[w0 + 256 * k] = v[k];
+    }
+}
+
+cudaError_t launch_pitch_words(const uint64_t* src, int64_t nw, uint64_t* dst, int64_t pitch, int64_t m, int num_sms,
+                               cudaStream_t stream) {
+    (void)num_sms;
+    const dim3 grid((unsigned)((nw + 2047) / 2048), (unsigned)(m < 65535 ? m : 65535));
+    pitch_words_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const unsigned long long*>(src), nw,
+                                                 reinterpret_cast<unsigned long long*>(dst), pitch, m);
+    return cudaGetLastError();
+}
+
 }  // namespace mib200

@@ -42,9 +42,9 @@ def both_paths(engine, words, n, fn):
     m = words.shape[0]
     w = engine.upload(words)
     with knobs(xp=1):
-        # the words' TMA map needs a row pitch of 16-byte multiples: odd word
-        # counts per column fall back to the unpack path
-        assert engine.words_operand(n, m) == (((n + 63) // 64) % 2 == 0)
+        # (odd word counts per column run on a padded copy: the TMA row pitch
+        # must be a multiple of 16 bytes)
+        assert engine.words_operand(n, m)
         a = fn(w)
     with knobs(xp=0):
         assert not engine.words_operand(n, m)
@@ -62,7 +62,7 @@ SHAPES = [
     (1, 1, 1.0), (300, 5, 0.5), (1000, 257, 0.3), (4099, 511, 0.5), (4200, 511, 0.5), (20_000, 700, 0.1),
     (129, 1, 0.5), (1_000_000, 100, 0.5),
     (70_001, 513, 0.45), (250_000, 256, 0.5), (600_000, 300, 0.02), (64 * 4 * 77 + 64, 600, 0.7),
-    # even word counts (the word-operand build runs): tiny m, m below one
+    # even word counts (no padded copy): tiny m, m below one
     # 128-row half, ragged K tails, tall N
     (128, 1, 0.5), (1024, 5, 0.7), (8192, 100, 0.2), (6400, 130, 0.5), (65_536 + 128, 255, 0.4),
     (1_000_064, 64, 0.5), (300_032, 1023, 0.05),
@@ -108,7 +108,7 @@ def test_tail_schedules(engine, tail, n, m):
 def test_output_forms_and_tile_subsets(engine):
     from paper_2411_19702_b200.engine import unpack_upper
 
-    n, m = 90_112, 1000  # an even word count: the word-operand build runs
+    n, m = 90_112, 1000
     rng = np.random.default_rng(17)
     words = O.pack_bits(rand_bits(rng, n, m, 0.25))
 
@@ -173,6 +173,8 @@ def test_default_rule_picks_words_for_narrow_m(engine):
     with knobs(xp=-1):
         assert engine.words_operand(8_000_000, 512)
         assert engine.words_operand(102_400, 2048)
+        assert engine.words_operand(8_000_064, 512)       # odd word count: padded copy, still ahead
+        assert not engine.words_operand(100_000, 2048)    # odd word count, wider: the unpack path
         assert not engine.words_operand(100_000, 10_000)
         assert not engine.words_operand((1 << 24) + 1, 256)  # int8 operands: no word build
 
