@@ -30,6 +30,19 @@
 // of B, and owns 128 accumulator rows.  CG == 1: 128x128 tiles on one SM
 // (int8 only).  TMEM: int8 -- two accumulators (double-buffered); e2m1 -- one
 // accumulator, a spare copy region and the block scales (see kSfCol below).
+//
+// Word-operand build (XP = true; tall-N / narrow-m): no X -- the operands are
+// expanded from the packed words inside the kernel.  Roles:
+//   warp 0            raw producer (one lane): TMA of packed words (16 words x
+//                     128 columns per operand half) into a 2-stage raw ring
+//   warp 1            MMA issuer: one warp-uniform loop over main tiles and the
+//                     tail unit; diagonal tiles read B from the A stage
+//   warps 2 .. 5      epilogue (E = 4); with xp_stats they first build the
+//                     T table and the column statistics (grid-wide barriers)
+//   warp 6            idle (the pacer slot)
+//   warps 7 .. 14     expanders, two groups of 4: raw stage -> swizzled e2m1
+//                     operand stages, proxy fence, relaxed arrive on the leader
+// (xp_put_row / xp stats: below).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
