@@ -455,8 +455,16 @@ struct TileWalk {
 // TMEM columns [256, 496), the last 16 into registers -- releases it (~10k
 // cycles instead of the ~80k of the whole epilogue), then computes from there.
 constexpr uint32_t kSfCol = 496;
-constexpr uint32_t kSpareCol = 256;
-constexpr int kSpareCols = 240;
+// e2m1: consecutive accumulators alternate between TMEM columns [0, 256) and
+// [kAltCol, kAltCol + 256) = [240, 496), which overlap in 16 columns only.  An
+// evacuating epilogue saves those 16 columns of its tile to registers and
+// releases the accumulator at once: the next tile's MMAs write the other
+// position while the epilogue reads the rest of its own straight from TMEM
+// (no copy: the old scheme copied 240 columns to a spare region first, ~5k
+// of a config-4 tile's ~136k cycles of MMA wait).  Accumulator k of a CTA pair
+// (main tiles, then the tail unit) sits at acc_col(k).
+constexpr uint32_t kAltCol = 240;
+__device__ __forceinline__ uint32_t acc_col(bool fp4, int k) { return (fp4 && (k & 1)) ? kAltCol : 0u; }
 template <int CG, bool FP4>
 __device__ __forceinline__ void mma_step(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t tmem_base, uint32_t acc) {
@@ -500,12 +508,12 @@ __device__ __noinline__ uint2 producer_tail(const CUtensorMap* tmap, int2 tile, 
 
 template <int CG, int ST, bool FP4>
 __device__ __noinline__ void mma_tail(uint32_t tmem_base, int width, int kb0, int kb1, uint32_t sA, uint32_t sB,
-                                      uint32_t bar0, int s, uint32_t ph, int acc, uint32_t aph) {
+                                      uint32_t bar0, int s, uint32_t ph, int acc, uint32_t aph, uint32_t acol) {
     using C = Cfg<CG, 8>;
-    const uint32_t idesc = mma_idesc<CG, FP4>(C::MMA_M, width);  // M x W accumulator in TMEM columns [0, W)
+    const uint32_t idesc = mma_idesc<CG, FP4>(C::MMA_M, width);  // M x W accumulator in columns [acol, acol + W)
     mbar_wait(bar0 + 8u * (2 * ST + 2 + acc), aph ^ 1u);  // tempty[acc]
     tc_fence_after();
-    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS) + acol;
     for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(bar0 + 8u * s, ph);  // full[s]
         tc_fence_after();
@@ -783,7 +791,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     const uint64_t bd = share ? adesc0 : bdesc0;
                     mbar_wait(tempty_bar(acc), aph ^ 1u);
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+                    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS) + acc_col(FP4, sg);
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(full_bar(s), ph);
                         tc_fence_after();
@@ -824,7 +832,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 tc_fence_after();
                 const bool trc = p.trace && cluster == 0 && it < 64;
                 if (trc && lane == 0) p.trace[it * 4 + 0] = clock64();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::ACC_COLS) + acc_col(FP4, it);
                 long long wait_cyc = 0;
                 for (int kb = 0; kb < nkb; ++kb) {
                     if (trc) {
@@ -861,7 +869,8 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 if (++acc == NACC) { acc = 0; aph ^= 1u; }
             }
             if (has_tail && lane == 0)
-                mma_tail<CG, ST, FP4>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph);
+                mma_tail<CG, ST, FP4>(tmem_base, tail_w, tail_kb0, tail_kb1, sA, sB, bar0, s, ph, acc, aph,
+                                      acc_col(FP4, it));
         }
     } else if (XP && (warp == 0 || warp >= C::PACER_WARP)) {
         // ================= word operands (XP) =================
@@ -1200,23 +1209,18 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             // the accumulator until done and run their epilogue alone.
             const bool EVAC = FP4 && TAIL == 0 && p.evac != 0 &&
                               (OUT == MI_OUT_COUNTS || use_table || use_hybrid || use_f32 || p.evac == 2);
-            uint32_t keep[16];  // EVAC: the accumulator columns that do not fit the spare TMEM
+            // this accumulator's TMEM columns, and (EVAC) the 16 of them the next
+            // accumulator overlaps (acc_col): saved here before the release
+            const uint32_t accb = acc_col(FP4, it);
+            const int ovl = accb ? 0 : C::TS - 16;
+            uint32_t keep[16];
             if (EVAC) {
-#pragma unroll 1
-                for (int c = 0; c < part_cols; c += 16) {
-                    const int col0 = part * part_cols + c;
-                    uint32_t r[16];
-                    tmem_ld_32x32b_x16(tmem_base + lane_q + (uint32_t)col0, r);
-                    tmem_ld_wait(r);
-                    if (col0 < kSpareCols) {
-                        tmem_st_32x32b_x16(tmem_base + lane_q + kSpareCol + (uint32_t)col0, r);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) keep[k] = r[k];
-                    }
+                if (ovl >= part * part_cols && ovl < (part + 1) * part_cols) {
+                    tmem_ld_32x32b_x16(tmem_base + lane_q + accb + (uint32_t)ovl, keep);
+                    tmem_ld_wait(keep);
                 }
-                tmem_st_wait();
-                // the accumulator is free: the next tile's MMAs start now
+                // the accumulator is free: the next tile's MMAs start now (on the
+                // other position)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(tempty_leader0);
@@ -1226,16 +1230,11 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 const int col0 = part * part_cols + c;   // accumulator column
                 const int j0 = tile.y * C::TS + c0 + col0;
                 uint32_t r[16];
-                if (EVAC) {
-                    if (col0 < kSpareCols) {
-                        tmem_ld_32x32b_x16(tmem_base + lane_q + kSpareCol + (uint32_t)col0, r);
-                        tmem_ld_wait(r);
-                    } else {
+                if (EVAC && col0 == ovl) {
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) r[k] = keep[k];
-                    }
+                    for (int k = 0; k < 16; ++k) r[k] = keep[k];
                 } else {
-                    tmem_ld_32x32b_x16(tmem_base + lane_q + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
+                    tmem_ld_32x32b_x16(tmem_base + lane_q + accb + (uint32_t)(acc * C::ACC_COLS + tc0 + col0), r);
                     tmem_ld_wait(r);
                 }
                 if (!(FP4 && use_f32 && TAIL != 2)) acc_to_counts<FP4>(r);  // (the f32 path reads fp32 counts as is)
@@ -1327,7 +1326,8 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
             for (int c = 0; c < C::WARP_COLS; c += 16) {
                 const int col0 = part * C::WARP_COLS + c;
                 uint32_t r[16];
-                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::ACC_COLS + col0), r);
+                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q * 32) << 16) + acc_col(FP4, it) +
+                                       (uint32_t)(acc * C::ACC_COLS + col0), r);
                 tmem_ld_wait(r);
                 acc_to_counts<FP4>(r);
                 uint4* dst = reinterpret_cast<uint4*>(dst_base + ((size_t)(col0 / 16) * 128 + row_local) * 16);
