@@ -137,6 +137,57 @@ def test_c_abi_rejects_bad_arguments_without_device_work():
     assert rc == nat.MI_ERR_DOMAIN and "padding" in nat.last_error()
 
 
+def test_words_operand_rule():
+    """The word-operand (XP) dispatch rule (capi_common.cu words_operand):
+    e2m1 operands only (N < 2^24), m_pad <= xp_cols, a third of that for an
+    odd word count per column; xp=0 never, xp=1 always (host logic)."""
+    lib = nat.lib()
+    old = {k: nat.get_tuning(k) for k in ("xp", "xp_cols")}
+    try:
+        nat.set_tuning(xp=-1, xp_cols=3072)
+        assert lib.mi_words_operand(8_000_000, 512) == 1        # even word count
+        assert lib.mi_words_operand(8_000_000, 3072) == 1
+        assert lib.mi_words_operand(8_000_000, 3073) == 0       # m_pad 3328 > 3072
+        assert lib.mi_words_operand(8_000_064, 512) == 1        # odd word count: m_pad <= 1024
+        assert lib.mi_words_operand(8_000_064, 1024) == 1
+        assert lib.mi_words_operand(8_000_064, 1025) == 0
+        assert lib.mi_words_operand(1 << 24, 512) == 0          # int8 operands beyond 2^24 rows
+        assert lib.mi_words_operand(50_000, 50_000) == 0        # config 4: the unpack path
+        nat.set_tuning(xp=0)
+        assert lib.mi_words_operand(8_000_000, 512) == 0
+        nat.set_tuning(xp=1)
+        assert lib.mi_words_operand(8_000_000, 50_000) == 1
+        assert lib.mi_words_operand(1 << 24, 512) == 0          # never without e2m1 operands
+    finally:
+        nat.set_tuning(**old)
+
+
+def test_new_entry_points_reject_bad_arguments_without_device_work():
+    """Word-operand, sparse-ingest and multi-device entry points validate
+    their arguments before any device call."""
+    lib = nat.lib()
+    rc = lib.mi_gram_mi_words(None, None, 100, 10, 0, 1e-12, 1, 1, None, 10, None, 1, None)
+    assert rc == nat.MI_ERR_DOMAIN and "required" in nat.last_error()
+    rc = lib.mi_gram_mi_words_stats(None, None, None, 100, 10, 0, 1e-12, 1, 1, None, 10, None, 1, None)
+    assert rc == nat.MI_ERR_DOMAIN
+    assert lib.mi_pack_sparse(None, None, 0, 10, None, None, None) == nat.MI_ERR_DIMENSION
+    assert lib.mi_pack_sparse(None, None, 10, 10, None, None, None) == nat.MI_ERR_DOMAIN
+    words = np.zeros((3, 1), dtype=np.uint64)
+    out = np.empty((3, 3))
+    devs = (ctypes.c_int * 2)(0, 1)
+    rc = lib.mi_all_pairs_host_devices(words.ctypes.data, 10, 3, 0, 1e-12, 1, 1, out.ctypes.data, None, 2)
+    assert rc == nat.MI_ERR_DOMAIN and "devices" in nat.last_error()
+    rc = lib.mi_all_pairs_host_devices(words.ctypes.data, 10, 3, 0, 1e-12, 1, 1, out.ctypes.data, devs, 0)
+    assert rc == nat.MI_ERR_DOMAIN
+    rc = lib.mi_all_pairs_host_devices(words.ctypes.data, 10, 3, 0, 1e-12, 1, 0, out.ctypes.data, devs, 2)
+    assert rc == nat.MI_ERR_DOMAIN and "counts" in nat.last_error()
+    rc = lib.mi_all_pairs_host_devices(words.ctypes.data, 0, 3, 0, 1e-12, 1, 1, out.ctypes.data, devs, 2)
+    assert rc == nat.MI_ERR_DIMENSION
+    dirty = np.array([[0b111]], dtype=np.uint64)  # padding bits set for n_rows = 2
+    rc = lib.mi_all_pairs_host_devices(dirty.ctypes.data, 2, 1, 0, 1e-12, 1, 1, out.ctypes.data, devs, 2)
+    assert rc == nat.MI_ERR_DOMAIN and "padding" in nat.last_error()
+
+
 def test_tuning_knobs_roundtrip():
     old = nat.get_tuning("band")
     nat.set_tuning(band=4)
