@@ -292,7 +292,9 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * (the word-operand build of mi_all_pairs_host and the Python engine: -1 auto
  * = when m_pad <= "xp_cols", default 3072 (a third of it for an odd word count
  * per column, which needs a padded copy); 0 never; 1 whenever the operands
- * are e2m1).  Also settable as MI_B200_<KEY> env vars. */
+ * are e2m1), "xp_diag_w" (word-operand build: cost of a diagonal tile in
+ * percent of an off-diagonal one, 10..100, which weights the K-range units of
+ * the last partial round; default 90).  Also settable as MI_B200_<KEY> env vars. */
 int mi_set_tuning(const char* key, int value);
 int mi_get_tuning(const char* key); /* -1 for an unknown key (and for "pace" = auto) */
 /* release the cached device workspaces of mi_*_host */

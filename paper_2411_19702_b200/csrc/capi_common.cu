@@ -64,7 +64,8 @@ Tuning& tuning() {
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
                        env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1), env_int("MI_B200_XP", -1),
-                       env_int("MI_B200_XP_COLS", 3072), env_int("MI_B200_XP_STATS", 1)};
+                       env_int("MI_B200_XP_COLS", 3072), env_int("MI_B200_XP_STATS", 1),
+                       env_int("MI_B200_XP_DIAG_W", 90)};
     return t;
 }
 int cta_group() { return tuning().cta_group; }
@@ -279,6 +280,9 @@ int mi_set_tuning(const char* key, int value) {
     } else if (!strcmp(key, "xp_stats")) {
         if (value != 0 && value != 1) return fail(MI_ERR_DOMAIN, "xp_stats must be 0 or 1");
         t.xp_stats = value;
+    } else if (!strcmp(key, "xp_diag_w")) {
+        if (value < 10 || value > 100) return fail(MI_ERR_DOMAIN, "xp_diag_w must be in [10, 100] (percent)");
+        t.xp_diag_w = value;
     } else if (!strcmp(key, "xp_cols")) {
         if (value < 0) return fail(MI_ERR_DOMAIN, "xp_cols must be >= 0");
         t.xp_cols = value;
@@ -316,6 +320,7 @@ int mi_get_tuning(const char* key) {
     if (!strcmp(key, "xp")) return t.xp;
     if (!strcmp(key, "debug")) return t.debug;
     if (!strcmp(key, "xp_cols")) return t.xp_cols;
+    if (!strcmp(key, "xp_diag_w")) return t.xp_diag_w;
     if (!strcmp(key, "xp_stats")) return t.xp_stats;
     return -1;
 }

@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "mi_kernels.h"
+
 namespace mib200 {
 namespace capi {
 
@@ -26,7 +28,7 @@ constexpr int kMaxIngestStages = 16;
 int env_int(const char* name, int dflt);
 struct Tuning {
     int cta_group, prefetch, l2_hint, band, stages, epi_warps, debug, fixed, table_thr, pace, tail, fp4, evac, shard,
-        hybrid, unperm_ctas, ingest, ingest_split, serp, f32_epi, xp, xp_cols, xp_stats;
+        hybrid, unperm_ctas, ingest, ingest_split, serp, f32_epi, xp, xp_cols, xp_stats, xp_diag_w;
 };
 // the word-operand build (mi_words_operand's rule)
 bool words_operand(int64_t n_rows, int64_t n_cols);
@@ -63,8 +65,12 @@ std::vector<int32_t> rank_tiles(int64_t T, int rank, int world, int band);
 // ---- the fused kernel launch (launch.cu); tail plan shared with the host path
 struct TailPlan {
     int n_full, split, kmode, epi;
+    int units;                        // sum of cnt
+    unsigned char cnt[kTailMaxUnits];  // units of tail tile i
 };
-TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb);
+TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb, const int32_t* h_tiles = nullptr, int diag_w = 100,
+                   int epi_parts = 2);
+int tail_epi_parts(bool xp);  // epilogue warps per TMEM lane quadrant of the build
 int launch_fused(const int8_t* d_kmajor, const void* d_colstat, int64_t n_rows, int64_t n_cols, int64_t ld, int mode,
                  double epsilon, int include_diagonal, int out_kind, void* d_out, int64_t ld_out, const int32_t* d_tiles,
                  int64_t n_tiles, unsigned int* row_done, cudaStream_t stream, const uint64_t* d_words = nullptr,

@@ -636,15 +636,23 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
     const int nkb = p.num_k_blocks;
     const TileWalk walk{cluster, n_clusters, p.n_full, nkb, p.serp & 1};
     // this cluster's split tail unit, if any
-    const int n_tail_units = (p.n_tiles - p.n_full) * p.tail_split;
-    const bool has_tail = p.tail_split > 1 && cluster < n_tail_units;
-    const int tail_t = has_tail ? p.n_full + cluster / p.tail_split : 0;
-    const int tail_c = has_tail ? cluster % p.tail_split : 0;
+    // tail tile i runs units [u0, u0 + tail_cnt[i]) (consecutive clusters)
+    const int n_tail = p.tail_split > 1 ? p.n_tiles - p.n_full : 0;
+    int tail_i = 0, tail_u0 = 0;
+    for (; tail_i < n_tail; ++tail_i) {
+        const int c = p.tail_cnt[tail_i];
+        if (cluster < tail_u0 + c) break;
+        tail_u0 += c;
+    }
+    const bool has_tail = tail_i < n_tail;
+    const int tail_s = has_tail ? (int)p.tail_cnt[tail_i] : 1;  // units of this cluster's tail tile
+    const int tail_t = has_tail ? p.n_full + tail_i : 0;
+    const int tail_c = has_tail ? cluster - tail_u0 : 0;
     const bool tail_k = has_tail && p.tail_kmode != 0;
     // N mode: MMA slice width; K mode: full width, K range [kb0, kb1), epilogue slice tail_we
-    const int tail_w = (has_tail && !tail_k) ? C::TS / p.tail_split : C::TS;
-    const int tail_kb0 = tail_k ? (int)((long long)tail_c * nkb / p.tail_split) : 0;
-    const int tail_kb1 = tail_k ? (int)((long long)(tail_c + 1) * nkb / p.tail_split) : nkb;
+    const int tail_w = (has_tail && !tail_k) ? C::TS / tail_s : C::TS;
+    const int tail_kb0 = tail_k ? (int)((long long)tail_c * nkb / tail_s) : 0;
+    const int tail_kb1 = tail_k ? (int)((long long)(tail_c + 1) * nkb / tail_s) : nkb;
     const int tail_we = tail_k ? C::TS / p.tail_epi : tail_w;
     // L2 pacing: every pair walks K at the same rate over tiles drawn from a few
     // shared column blocks; kept within a window of one another, the pairs read
@@ -1086,8 +1094,15 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                         p.xlogx_w[c] = fix_xlog2x((unsigned)c, p.fix_s, kFixR, kFixLG);
                 volatile unsigned int* sync = p.xp_sync;
                 if (etid == 0) {
+                    // completions to wait for: every expander warp of every diagonal tile's units
+                    unsigned int expect = 0;
+                    for (int i = 0; i < n_tail; ++i) {
+                        const int2 tl = p.tiles[p.n_full + i];
+                        if (tl.x == tl.y) expect += p.tail_cnt[i];
+                    }
+                    expect *= (unsigned)(CG * kXpWarps);
                     const long long t0 = clock64();
-                    while (sync[0] < p.xp_diag_expect) {
+                    while (sync[0] < expect) {
                         __nanosleep(256);
                         if (clock64() - t0 > (1ll << 36)) __trap();  // a lost unit is a bug
                     }
@@ -1239,23 +1254,29 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 }
                 if (!(FP4 && use_f32 && TAIL != 2)) acc_to_counts<FP4>(r);  // (the f32 path reads fp32 counts as is)
                 if constexpr (TAIL == 2) {  // + the other K ranges (integer adds: exact in any order)
-                    const int u0 = (t - p.n_full) * p.tail_split;
                     const size_t off = ((size_t)((tc0 + col0) / 16) * 128 + row_local) * 16;
+                    // kTailSumDepth partials in flight per step (a unit sums up to ~74 of them)
 #pragma unroll 1
-                    for (int w = 0; w < p.tail_split; ++w) {
-                        if (w == tail_c) continue;
-                        const uint4* src = reinterpret_cast<const uint4*>(
-                            p.tail_part + (size_t)((u0 + w) * CG + (int)rank) * 128 * C::TS + off);
-                        uint4 x[4];
+                    for (int w0 = 0; w0 < tail_s; w0 += kTailSumDepth) {
+                        uint4 x[kTailSumDepth][4];
 #pragma unroll
-                        for (int k4 = 0; k4 < 4; ++k4) x[k4] = __ldcg(src + k4);
+                        for (int j = 0; j < kTailSumDepth; ++j) {
+                            const int w = w0 + j;
+                            const bool use = w < tail_s && w != tail_c;
+                            const uint4* src = reinterpret_cast<const uint4*>(
+                                p.tail_part + (size_t)((tail_u0 + (use ? w : 0)) * CG + (int)rank) * 128 * C::TS + off);
 #pragma unroll
-                        for (int k4 = 0; k4 < 4; ++k4) {
-                            r[4 * k4 + 0] += x[k4].x;
-                            r[4 * k4 + 1] += x[k4].y;
-                            r[4 * k4 + 2] += x[k4].z;
-                            r[4 * k4 + 3] += x[k4].w;
+                            for (int k4 = 0; k4 < 4; ++k4) x[j][k4] = use ? __ldcg(src + k4) : make_uint4(0u, 0u, 0u, 0u);
                         }
+#pragma unroll
+                        for (int j = 0; j < kTailSumDepth; ++j)
+#pragma unroll
+                            for (int k4 = 0; k4 < 4; ++k4) {
+                                r[4 * k4 + 0] += x[j][k4].x;
+                                r[4 * k4 + 1] += x[j][k4].y;
+                                r[4 * k4 + 2] += x[j][k4].z;
+                                r[4 * k4 + 3] += x[j][k4].w;
+                            }
                     }
                 }
                 const bool vec_ok = ((reinterpret_cast<uintptr_t>(o + (int64_t)i * ldd + j0) & (2 * sizeof(T) - 1)) == 0);
@@ -1345,7 +1366,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                 if (etid == 0) {
                     volatile unsigned int* f = flag;
                     const long long t0 = clock64();
-                    while (*f < (unsigned int)p.tail_split) {
+                    while (*f < (unsigned int)tail_s) {
                         __nanosleep(64);
                         if (clock64() - t0 > (1ll << 36)) __trap();  // ~30 s: a lost unit is a bug
                     }
@@ -1381,9 +1402,12 @@ cudaError_t launch_impl(const CUtensorMap& tmap, const GramMiParams& p, int num_
     const int max_clusters = num_sms / CG;
     int clusters = p.n_tiles < max_clusters ? p.n_tiles : max_clusters;
     if (p.tail_split > 1) {  // the host sized n_full as a multiple of max_clusters
-        if (p.n_full % max_clusters != 0 || (p.n_tiles - p.n_full) * p.tail_split > max_clusters)
+        int units = 0;
+        for (int i = 0; i < p.n_tiles - p.n_full; ++i) units += p.tail_cnt[i];
+        if (p.n_full % max_clusters != 0 || p.n_tiles - p.n_full > kTailMaxUnits || units != p.tail_units ||
+            units > max_clusters)
             return cudaErrorInvalidValue;
-        clusters = p.n_full > 0 ? max_clusters : (p.n_tiles - p.n_full) * p.tail_split;
+        clusters = p.n_full > 0 ? max_clusters : units;
     }
     if (clusters < 1) clusters = 1;
     cudaLaunchConfig_t cfg = {};

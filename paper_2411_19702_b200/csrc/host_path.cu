@@ -561,7 +561,9 @@ int all_pairs_host_impl(const uint64_t* h_words, int64_t n_rows, int64_t n_cols,
     {
         const std::vector<int32_t> tl = all_tiles(T, tile_band(), 1);
         const int64_t nt = (int64_t)tl.size() / 2;
-        const TailPlan tp = tail_plan(nt, (int)cg, info.num_sms / (int)cg, (int)(mi_kmajor_ld(n_rows) / 128));
+        const TailPlan tp = tail_plan(nt, (int)cg, info.num_sms / (int)cg, (int)(mi_kmajor_ld(n_rows) / 128), tl.data(),
+                                      words_operand(n_rows, n_cols) ? tuning().xp_diag_w : 100,
+                                      tail_epi_parts(words_operand(n_rows, n_cols)));
         for (int64_t k = 0; k < nt; ++k) expect[(size_t)tl[2 * k]] += cg * (k >= tp.n_full ? (unsigned)tp.epi : 1u);
     }
     if ((rc = run_fused(*ws, n_rows, n_cols, ld, m_pad, mode, epsilon, include_diagonal, out_kind, ws->out,

@@ -50,33 +50,76 @@ int pace_window(int64_t n_tiles, int nkb, int num_sms) {
 }
 
 // Tail split of the last partial round (GramMiParams::tail_*): its r tiles
-// become s units each so that r * s of the clusters share it instead of r.
+// become units so that the clusters share it instead of r of them.
 // Short K (< kTailKMinKb k-blocks; latency-bound): column slices of the tile
 // with the full K range, s a power of two, slices >= 32 wide.  Long K (the
 // slices would be load-bound: a narrow MMA still streams a full A block):
-// K ranges of the full tile, s = clusters / r, whose int32 partials are summed
-// by e <= s epilogue units, one column slice each (config 3: 820 tiles = 11
-// rounds of 74 + 6; the 6 run as 72 K ranges, summed by 48 epilogue slices).
+// K ranges of the full tile, every cluster used: tile i gets s_i units, dealt
+// one at a time to the tile whose units would run longest (w_i / s_i, w_i its
+// cost weight; equal weights give counts that differ by at most one), and
+// the int32 partials of a tile are summed by e <= min s_i epilogue units, one
+// column slice each, at least 16 columns per epilogue warp (epi_parts warps
+// share a TMEM lane quadrant; config 3: 820 tiles = 11 rounds of 74 + 6; the
+// 6 run as 74 K ranges, summed by 8 epilogue slices each).  Weights: `h_tiles` (the
+// host copy of the launch's tile list, or nullptr) marks the diagonal tail
+// tiles, which cost diag_w percent of an off-diagonal one (the word-operand
+// build stages one operand copy for them; knob "xp_diag_w").
 // Knob "tail": 0 off, 1 auto, 2 slices only, 3 K ranges only.
 constexpr int kTailKMinKb = 256;
-TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb) {
-    TailPlan tp{(int)n_tiles, 1, 0, 1};
+int tail_epi_parts(bool xp) { return (xp ? kXpEpiWarps : tuning().epi_warps) / 4; }
+TailPlan tail_plan(int64_t n_tiles, int cg, int clusters, int nkb, const int32_t* h_tiles, int diag_w, int epi_parts) {
+    TailPlan tp{};
+    tp.n_full = (int)n_tiles;
+    tp.split = 1;
+    tp.kmode = 0;
+    tp.epi = 1;
+    tp.units = 0;
     const int mode = tuning().tail;
     if (!mode || clusters < 2) return tp;
     const int64_t r = n_tiles % clusters;
-    if (r == 0) return tp;
+    if (r == 0 || r > kTailMaxUnits) return tp;
     const bool kmode = mode == 3 || (mode == 1 && nkb >= kTailKMinKb);
     int s = 1, e = 1;
     while (e * 2 * 32 <= 128 * cg && r * e * 2 <= clusters) e *= 2;  // power-of-two column slices
+    if (kmode) {  // epilogue slices: 16 columns per epilogue warp column part at least
+        e = 1;
+        while (e * 2 * 16 * epi_parts <= 128 * cg) e *= 2;
+    }
+    const int cap = std::min(std::min(nkb, kTailMaxUnits), 255);
     if (kmode) {
-        s = (int)(clusters / r);
-        if (s > nkb) s = nkb;
-        if (s > kTailMaxUnits) s = kTailMaxUnits;
-        while (e > s) e /= 2;  // epilogue slices stay a power of two
+        if (clusters / r < 2 || cap < 2) return tp;
+        const int budget = std::min(clusters, kTailMaxUnits);
+        int w[kTailMaxUnits];
+        int used = 0;
+        for (int i = 0; i < (int)r; ++i) {
+            const int64_t t = n_tiles - r + i;
+            const bool diag = h_tiles && h_tiles[2 * t] == h_tiles[2 * t + 1];
+            w[i] = diag ? std::max(1, std::min(diag_w, 100)) : 100;
+            tp.cnt[i] = 2;
+            used += 2;
+        }
+        for (; used < budget; ++used) {  // the next unit to the tile whose units run longest
+            int best = -1;
+            for (int i = 0; i < (int)r; ++i)
+                if (tp.cnt[i] < cap && (best < 0 || (int64_t)w[i] * tp.cnt[best] > (int64_t)w[best] * tp.cnt[i]))
+                    best = i;
+            if (best < 0) break;
+            ++tp.cnt[best];
+        }
+        s = 2;
+        int smin = cap;
+        for (int i = 0; i < (int)r; ++i) {
+            s = std::max(s, (int)tp.cnt[i]);
+            smin = std::min(smin, (int)tp.cnt[i]);
+        }
+        while (e > smin) e /= 2;  // epilogue slices stay a power of two
+        tp.units = used;
     } else {
         s = e;
+        if (s < 2 || r * s > kTailMaxUnits) return tp;
+        for (int i = 0; i < (int)r; ++i) tp.cnt[i] = (unsigned char)s;
+        tp.units = (int)(r * s);
     }
-    if (s < 2 || r * s > kTailMaxUnits) return tp;
     tp.n_full = (int)(n_tiles - r);
     tp.split = s;
     tp.kmode = kmode ? 1 : 0;
@@ -503,9 +546,19 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     p.pace = nullptr;
     p.pace_window = xp ? 0 : pace_window(n_tiles, p.num_k_blocks, info.num_sms);
     if (p.pace_window > 0 && (rc = pace_slots(dev, &p.pace))) return rc;
-    const TailPlan tp = tail_plan(n_tiles, cta_group(), info.num_sms / cta_group(), p.num_k_blocks);
+    // the diagonal tail tiles (cost weights of the K-range units): known for
+    // the full list in the order the engine and the host paths build it (a
+    // heuristic -- any order and any counts give the same results)
+    std::vector<int32_t> canon;
+    const int64_t T_side = tiles_per_side(n_cols);
+    if (xp && n_tiles == T_side * (T_side + 1) / 2) canon = all_tiles(T_side, tile_band(), row_done ? 1 : 0);
+    const TailPlan tp = tail_plan(n_tiles, cta_group(), info.num_sms / cta_group(), p.num_k_blocks,
+                                  canon.empty() ? nullptr : canon.data(), xp ? tuning().xp_diag_w : 100,
+                                  tail_epi_parts(xp));
     p.n_full = tp.n_full;
     p.tail_split = tp.split;
+    p.tail_units = tp.units;
+    memcpy(p.tail_cnt, tp.cnt, sizeof(p.tail_cnt));
     p.tail_kmode = tp.kmode;
     p.tail_epi = tp.epi;
     p.tail_flag = nullptr;
@@ -539,7 +592,6 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
     // diagonal units' columns), else by kernel 1's counting pass first
     p.xp_stats = 0;
     p.xp_sync = nullptr;
-    p.xp_diag_expect = 0;
     p.colstat_w = reinterpret_cast<ColStat*>(const_cast<void*>(d_colstat));
     p.colsum = d_colsum;
     p.blkrange_w = blkrange_ptr(const_cast<void*>(d_colstat), n_rows, n_cols);
@@ -557,7 +609,6 @@ int mib200::capi::launch_fused(const int8_t* d_kmajor, const void* d_colstat, in
             MI_CUDA(launch_unpack_prep(n_rows, mi_kmajor_rows(n_cols), cs, xl, br, fr, info.num_sms, stream, false));
             MI_CUDA(cudaMemsetAsync(p.xp_sync, 0, 2 * sizeof(unsigned int), stream));
             p.xp_stats = 1;
-            p.xp_diag_expect = (unsigned)(T * tp.split * cta_group() * kXpWarps);
             p.xlogx_w = xl;
         } else {
             MI_CUDA(launch_unpack_colsum(d_words, n_rows, n_cols, (n_rows + 63) / 64, xp ? nullptr : (int8_t*)d_kmajor,

@@ -15,6 +15,9 @@ namespace mib200 {
 
 struct ColStat;
 
+constexpr int kTailMaxUnits = 148;      // split tail units (<= clusters): flag pairs and partial slots
+constexpr int kTailSumDepth = 4;        // K-range tail: other units' partials loaded per step of the sum
+
 struct GramMiParams {
     const ColStat* colstat; // [m_pad] per-column marginals (kernel 1)
     const int2* tiles;      // [n_tiles] (I, J) tile coordinates, I <= J
@@ -52,21 +55,26 @@ struct GramMiParams {
     unsigned int* pace;     // optional: per-cluster k-block progress, stride kPaceStride (L2 pacing)
     int pace_window;        // leader producers stay within this many k-blocks of the slowest pair (0 = off)
     // Tail split of the last, partial round: tiles [0, n_full) are dealt
-    // whole, round robin; each of the n_tiles - n_full tail tiles becomes
-    // tail_split units run by clusters u = (t - n_full) * tail_split + c:
+    // whole, round robin; tail tile i = t - n_full becomes s_i = tail_cnt[i]
+    // units, run by consecutive clusters u = u0_i + c (u0_i = the counts
+    // before it; tail_units = their sum):
     //  tail_kmode 0 (short K): unit c = column slice [c W, (c + 1) W) of the
-    //    tile with the full K range, W = TS / tail_split -- no partial sums;
+    //    tile with the full K range, W = TS / s_i (all s_i = tail_split) --
+    //    no partial sums;
     //  tail_kmode 1 (long K; a narrow slice would be load-bound): unit c = K
-    //    range c of the full tile.  Every unit stores its int32 accumulator in
-    //    tail_part (slot u, 128 x TS per CTA) and bumps tail_flag[(t - n_full)
-    //    * 2 + rank] (zeroed by the host before the launch); units c <
-    //    tail_epi then wait for all tail_split partials and run the epilogue
-    //    of column slice c (TS / tail_epi wide) on their sum.
+    //    range c of s_i of the full tile (s_i may differ per tile: weighted by
+    //    tile cost).  Every unit stores its int32 accumulator in tail_part
+    //    (slot u, 128 x TS per CTA) and bumps tail_flag[i * 2 + rank] (zeroed
+    //    by the host before the launch); units c < tail_epi (<= every s_i)
+    //    then wait for all s_i partials and run the epilogue of column slice c
+    //    (TS / tail_epi wide) on their sum.
+    int tail_units;
+    unsigned char tail_cnt[kTailMaxUnits];
     int serp;               // 1: odd tile rounds sweep K backwards (L2 reuse across rounds)
     int evac;               // fp4: evacuate the accumulator before the epilogue (0 off, 1 FP64-free
                             // epilogues, 2 always)
     int n_full;
-    int tail_split;         // 1 = no split
+    int tail_split;         // 1 = no split, else the largest tail_cnt
     int tail_kmode;
     int tail_epi;
     unsigned int* tail_flag;
@@ -84,7 +92,6 @@ struct GramMiParams {
     // column statistics and meet at a grid-wide barrier before any epilogue.
     int xp_stats;
     unsigned int* xp_sync;        // [0] diagonal expander-warp completions, [1] CTAs done (zeroed by the host)
-    unsigned int xp_diag_expect;  // completions [0] must reach
     ColStat* colstat_w;           // writable alias of colstat
     int32_t* colsum;              // optional column-sum output
     int2* blkrange_w;             // writable alias of blkrange
@@ -96,7 +103,6 @@ constexpr int kXpEpiWarps = 4;          // word-operand build: epilogue warps
 constexpr int kXpStages = 4;            // word-operand build: operand ring depth (a raw-word ring sits in front)
 constexpr int kPaceStride = 8;          // u32 per cluster slot (one 32-B sector each)
 constexpr int kPaceMaxClusters = 256;
-constexpr int kTailMaxUnits = 148;      // split tail units (<= clusters): flag pairs and partial slots
 constexpr long long kXlogxMaxN = 1ll << 24;  // table path: N < 2^24 (8 (N + 1) bytes)
 constexpr int kFixLogBitsH = 10;             // = kFixLogBits (fixlog_table.h), for host code
 constexpr long long kFixTabBytes = (1ll << kFixLogBitsH) * 12;  // kFixR floats + kFixLG float2s
