@@ -500,6 +500,12 @@ def run_gpu(args):
         "kernel_ms": kern_ms,
         "kernel_share_of_step": kern_ms / step_ms,
     }
+    # the same fraction at the SM clock the timed region actually ran at: the
+    # peak is MACs/clk/SM x SMs x clock, and a power-capped step (sw_power_cap)
+    # runs below the clock the MMA-only probe holds
+    if clocks and clocks.get("sm_mhz") and peak_burst.get("sm_mhz"):
+        roofline["sm_mhz_timed_region"] = clocks["sm_mhz"]
+        roofline["frac_at_timed_clock"] = roofline["frac"] * peak_burst["sm_mhz"] / clocks["sm_mhz"]
 
     e2e = None
     if not args.no_e2e:

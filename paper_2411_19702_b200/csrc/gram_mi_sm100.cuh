@@ -689,9 +689,15 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
         // issues.  Under a concurrent epilogue the producer and MMA warps get
         // a fraction of their schedulers' issue slots, so the per-k-block
         // instruction path is kept short.
-        const uint64_t policy = p.l2_hint == 1   ? l2_policy_evict_last()
-                                : p.l2_hint == 2 ? l2_policy_evict_first()
-                                                 : l2_policy_evict_normal();
+        const uint64_t policy = (p.l2_hint == 1 || p.l2_hint >= 3) ? l2_policy_evict_last()
+                                : p.l2_hint == 2                   ? l2_policy_evict_first()
+                                                                   : l2_policy_evict_normal();
+        // l2_hint 3 / 4: the row-block operand (the same for every round of a
+        // band) keeps evict_last, the column-block operand (new every round)
+        // loads evict_first / unchanged
+        const uint64_t policy_b = p.l2_hint == 3   ? l2_policy_evict_first()
+                                  : p.l2_hint == 4 ? l2_policy_evict_normal()
+                                                   : policy;
         const int pf = p.prefetch_dist;
         const uint32_t fb_rank = (CG == 2) ? 0u : rank;  // CG == 2: signal the leader's barrier
         int s = 0;
@@ -755,7 +761,7 @@ gram_mi_kernel(const __grid_constant__ CUtensorMap tmap_x, const GramMiParams p)
                     const uint32_t fb = (CG == 2) ? map_to_cta(full_bar(s), fb_rank) : full_bar(s);
                     if (rank == 0) mbar_arrive_expect_tx(full_bar(s), C::STAGE_TX);
                     tma_load_3d<CG>(sA + s * kStageHalfBytes, &tmap_x, fb, 0, rowA, kb, policy);
-                    tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy);
+                    tma_load_3d<CG>(sB + s * kStageHalfBytes, &tmap_x, fb, 0, rowB, kb, policy_b);
                 }
                 __syncwarp();
                 if (++s == ST) { s = 0; ph ^= 1u; }
