@@ -269,8 +269,7 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
 
 /* Tuning knobs (process-wide): "cta_group" (2 = 256x256 tiles on an SM pair,
  * 1 = 128x128 on one SM), "prefetch" (L2 prefetch distance in k-blocks),
- * "l2_hint" (0 normal, 1 evict_last, 2 evict_first, 3 / 4 row blocks evict_last +
- * column blocks evict_first / normal), "band" (tile rows per
+ * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per
  * band of the tile order), "stages" (smem ring depth), "epi_warps" (8 or 16
  * epilogue warps), "fixed" (exact-mode epilogue: 1 adaptive per tile, default;
  * 0 FP64 only; 2 fixed-point table only; 3 hybrid only), "table_thr" (adaptive threshold on

@@ -225,7 +225,7 @@ int mi_set_tuning(const char* key, int value) {
         if (value < 0 || value > 256) return fail(MI_ERR_DOMAIN, "prefetch must be in [0, 256]");
         t.prefetch = value;
     } else if (!strcmp(key, "l2_hint")) {
-        if (value < 0 || value > 4) return fail(MI_ERR_DOMAIN, "l2_hint must be 0 .. 4");
+        if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "l2_hint must be 0, 1 or 2");
         t.l2_hint = value;
     } else if (!strcmp(key, "band")) {
         if (value < 1) return fail(MI_ERR_DOMAIN, "band must be >= 1");

@@ -29,10 +29,31 @@ def timed(fn, reps=5):
     return sorted(t)[len(t) // 2]
 
 
-for spec in ["default"] + sys.argv[2:]:
-    kv = {} if spec == "default" else {k: int(v) for k, v in (x.split("=") for x in spec.split(","))}
-    old = {k: nat.get_tuning(k) for k in kv}
-    nat.set_tuning(**kv)
-    ms = timed(lambda: eng.compute(prep, None, dt, tiles=tl, out=out, tile_major=True))
-    nat.set_tuning(**old)
-    print(f"config {cfg} {spec}: fused {ms:.3f} ms", flush=True)
+def clock_mhz():
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        return pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:
+        return -1
+
+
+# Round robin over the settings (ROUNDS passes, 3 launches each): a power-capped
+# GPU slows down over the first seconds of load, so settings measured one after
+# another are not comparable (the first one runs ~10% faster at config 4).
+specs = ["default"] + sys.argv[2:]
+rounds = int(os.environ.get("ROUNDS", "3"))
+res = {sp: [] for sp in specs}
+for r in range(rounds):
+    for spec in specs:
+        kv = {} if spec == "default" else {k: int(v) for k, v in (x.split("=") for x in spec.split(","))}
+        old = {k: nat.get_tuning(k) for k in kv}
+        nat.set_tuning(**kv)
+        ms = timed(lambda: eng.compute(prep, None, dt, tiles=tl, out=out, tile_major=True), reps=3)
+        nat.set_tuning(**old)
+        res[spec].append(ms)
+        print(f"  round {r} config {cfg} {spec}: fused {ms:.3f} ms (SM {clock_mhz()} MHz after)", flush=True)
+for spec in specs:
+    v = sorted(res[spec])
+    print(f"config {cfg} {spec}: fused median {v[len(v) // 2]:.3f} ms, min {v[0]:.3f}", flush=True)
