@@ -269,7 +269,8 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
 
 /* Tuning knobs (process-wide): "cta_group" (2 = 256x256 tiles on an SM pair,
  * 1 = 128x128 on one SM), "prefetch" (L2 prefetch distance in k-blocks),
- * "l2_hint" (0 normal, 1 evict_last, 2 evict_first), "band" (tile rows per
+ * "l2_hint" (0 normal, 1 evict_last, 2 evict_first, 3 / 4 row blocks evict_last +
+ * column blocks evict_first / normal), "band" (tile rows per
  * band of the tile order), "stages" (smem ring depth), "epi_warps" (8 or 16
  * epilogue warps), "fixed" (exact-mode epilogue: 1 adaptive per tile, default;
  * 0 FP64 only; 2 fixed-point table only; 3 hybrid only), "table_thr" (adaptive threshold on
@@ -286,7 +287,7 @@ int mi_bmi_load(const char* path, uint64_t* d_words, int64_t n_rows, int64_t n_c
  * (mi_all_pairs_host: S = 1..16 column groups uploaded, unpacked, computed and
  * copied back in a pipeline, default 4; 0 = one upload, row-band egress),
  * "ingest_split" (0 = even group sizes, default; 1 = doubling), "serp" (1 =
- * odd tile rounds sweep K backwards for L2 reuse across rounds; 0 default),
+ * odd tile rounds sweep K backwards for L2 reuse across rounds, default; 0 = always forwards),
  * "f32_epi" (float32 output, exact mode: tiles off the table path run the
  * FP32-pipe epilogue beside the next tile's MMAs; 1 default, 0 = FP64), "xp"
  * (the word-operand build of mi_all_pairs_host and the Python engine: -1 auto

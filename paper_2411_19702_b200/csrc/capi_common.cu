@@ -63,7 +63,7 @@ Tuning& tuning() {
                        env_int("MI_B200_EVAC", 1), env_int("MI_B200_SHARD", 1),
                        env_int("MI_B200_HYBRID", 0), env_int("MI_B200_UNPERM_CTAS", 0),
                        env_int("MI_B200_INGEST", 4), env_int("MI_B200_INGEST_SPLIT", 0),
-                       env_int("MI_B200_SERP", 0), env_int("MI_B200_F32_EPI", 1), env_int("MI_B200_XP", -1),
+                       env_int("MI_B200_SERP", 1), env_int("MI_B200_F32_EPI", 1), env_int("MI_B200_XP", -1),
                        env_int("MI_B200_XP_COLS", 3072), env_int("MI_B200_XP_STATS", 1),
                        env_int("MI_B200_XP_DIAG_W", 90)};
     return t;
@@ -225,7 +225,7 @@ int mi_set_tuning(const char* key, int value) {
         if (value < 0 || value > 256) return fail(MI_ERR_DOMAIN, "prefetch must be in [0, 256]");
         t.prefetch = value;
     } else if (!strcmp(key, "l2_hint")) {
-        if (value < 0 || value > 2) return fail(MI_ERR_DOMAIN, "l2_hint must be 0, 1 or 2");
+        if (value < 0 || value > 4) return fail(MI_ERR_DOMAIN, "l2_hint must be 0 .. 4");
         t.l2_hint = value;
     } else if (!strcmp(key, "band")) {
         if (value < 1) return fail(MI_ERR_DOMAIN, "band must be >= 1");

@@ -32,7 +32,7 @@ struct GramMiParams {
     double eps;
     int include_diagonal;
     int prefetch_dist;      // k-blocks of L2 prefetch ahead of the TMA ring (0 = off)
-    int l2_hint;            // 0 normal, 1 evict_last, 2 evict_first for operand loads
+    int l2_hint;            // operand loads: 0 normal, 1 evict_last, 2 evict_first, 3 / 4 rows evict_last + columns evict_first / normal
     int debug;              // experiments only (bit mask): 1 = compute but skip the output stores,
                             // 2 = skip the mirror stores, 4 = skip the direct stores, 8 = L2
                             // evict_first hint on the output stores, 16 = no MMAs (data movement only);

@@ -148,7 +148,7 @@ KNOB_VARIANTS = [
     {"tail": 0}, {"tail": 0, "pace": 16}, {"tail": 0, "cta_group": 1},
     {"tail": 2}, {"tail": 3}, {"tail": 3, "cta_group": 1}, {"tail": 2, "cta_group": 1}, {"tail": 3, "pace": 16},
     {"fp4": 0}, {"fp4": 0, "tail": 3}, {"fp4": 0, "pace": 16}, {"fp4": 0, "fixed": 0},
-    {"fixed": 3}, {"hybrid": 0}, {"fixed": 3, "fp4": 0}, {"serp": 1}, {"serp": 1, "pace": 16},
+    {"fixed": 3}, {"hybrid": 0}, {"fixed": 3, "fp4": 0}, {"serp": 0}, {"serp": 0, "pace": 16}, {"serp": 1},
     {"xp": 0}, {"xp": 1}, {"xp": 1, "tail": 3}, {"xp": 1, "tail": 2}, {"xp": 1, "fixed": 0}, {"xp": 1, "evac": 0},
 ]
 
@@ -362,12 +362,13 @@ def test_serpentine_k_order_is_bit_identical(engine):
     dens = rng.uniform(0.02, 0.98, m)
     words = O.pack_bits((rng.random((n, m)) < dens[None, :]).astype(np.uint8))
     res = {}
+    old = nat.get_tuning("serp")
     for sp in (0, 1):
         nat.set_tuning(serp=sp)
         try:
             res[sp] = (gpu_counts(engine, words, n)[0], gpu_mi(engine, words, n))
         finally:
-            nat.set_tuning(serp=0)
+            nat.set_tuning(serp=old)
     assert np.array_equal(res[0][0], res[1][0])
     assert np.array_equal(res[0][1], res[1][1])
     assert np.array_equal(res[1][0], O.c_gram_ones(words))

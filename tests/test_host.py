@@ -291,7 +291,7 @@ def test_every_documented_knob_round_trips():
 
     good = {"cta_group": 1, "prefetch": 4, "l2_hint": 0, "band": 3, "stages": 6, "epi_warps": 8, "fixed": 0,
             "table_thr": 1000, "pace": 16, "tail": 2, "fp4": 0, "evac": 2, "shard": 0, "hybrid": 1,
-            "unperm_ctas": 2, "ingest": 6, "ingest_split": 1, "serp": 1, "xp_diag_w": 75}
+            "unperm_ctas": 2, "ingest": 6, "ingest_split": 1, "serp": 0, "xp_diag_w": 75}
     bad = {"ingest": 17, "ingest_split": 2, "serp": 2, "unperm_ctas": 5, "evac": 3, "tail": 4, "xp_diag_w": 5}
     old = {k: nat.get_tuning(k) for k in good}
     try:

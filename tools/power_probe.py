@@ -42,11 +42,14 @@ def run(fn):
     a.record(); fn(); b.record(); b.synchronize()
     reps = max(3, int(seconds * 1e3 / a.elapsed_time(b)))
     s = Sampler(); s.start()
+    e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)  # mJ
     a.record()
     for _ in range(reps):
         fn()
     b.record(); b.synchronize()
+    e1 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
     s.on = False; s.join()
+    run.joules = (e1 - e0) / 1e3 / reps
     k = len(s.p) // 2  # second half: the controller has settled
     p2, c2 = s.p[k:], sorted(s.c[k:])
     return a.elapsed_time(b) / reps, sum(p2) / max(len(p2), 1), c2[len(c2) // 2] if c2 else -1
@@ -60,5 +63,5 @@ for spec in ["default"] + sys.argv[3:]:
     nat.set_tuning(**kv)
     ms, pw, mhz = run(lambda: eng.compute(prep, None, dt, tiles=tl, out=out, tile_major=True))
     nat.set_tuning(**old)
-    print(f"config {cfg} {spec}: {ms:.3f} ms/launch, {pw:.0f} W, SM {mhz} MHz -> {ms * mhz * 1e3 / 1e6:.2f} Mcycles", flush=True)
+    print(f"config {cfg} {spec}: {ms:.3f} ms/launch, {pw:.0f} W, SM {mhz} MHz -> {ms * mhz * 1e3 / 1e6:.2f} Mcycles, {run.joules:.2f} J/launch", flush=True)
     time.sleep(3.0)
