@@ -407,6 +407,10 @@ __device__ __forceinline__ void epilogue16(const uint32_t (&r)[16], int i, int j
 // tiles evaluate (min, max) orientations so the two halves are bit-identical.
 // RAW: r holds the fp32 accumulator words themselves (exact integer counts),
 // else integer counts (K-split partial sums, int8 accumulators).
+#ifndef MI_F32_EPI_YIELD
+#define MI_F32_EPI_YIELD 1   // yield after every n-th element of the float32 epilogue (0 = never; experiments)
+#endif
+constexpr int kF32EpiYield = MI_F32_EPI_YIELD;
 template <bool DIAG, bool RAW>
 __device__ __forceinline__ void epilogue16_f32(const uint32_t (&r)[16], int i, int j0, const ColF& Af,
                                                const ColF* __restrict__ cols, const GramMiParams& p, float dN,
@@ -417,9 +421,36 @@ __device__ __forceinline__ void epilogue16_f32(const uint32_t (&r)[16], int i, i
     for (int k = 0; k < 16; ++k) {
         const float g = RAW ? __uint_as_float(r[k]) : __uint2float_rn(r[k]);  // exact: counts < 2^24
         const int j = j0 + k;
-        float x = (DIAG && j < i) ? f32_mi(g, cols[k], Af, dN, rN) : f32_mi(g, Af, cols[k], dN, rN);
+        float x;
+        if constexpr (DIAG) {
+            // (min, max) orientation by selecting the operands, not the call:
+            // the lanes on both sides of the diagonal share one instruction
+            // stream (two calls under a per-lane condition ran both: a 151 k
+            // cycle epilogue against 80 k, and a pair held up by it holds every
+            // pair up through the pacing window)
+            const bool sw = j < i;
+            const ColF B = cols[k];
+            ColF X = Af, Y = B;
+            if (sw) { X = B; Y = Af; }
+            x = f32_mi(g, X, Y, dN, rN);
+        } else {
+            x = f32_mi(g, Af, cols[k], dN, rN);
+        }
         if (DIAG && !p.include_diagonal && i == j) x = 0.0f;
         v[k] = x;
+        // Give the issue slot away after every element.  This epilogue is a
+        // dense FP32 stream (~200 instructions per element, most of them
+        // scheduled back to back with the no-yield hint), it runs beside the
+        // next tile's MMAs, and its 8 warps share the 4 schedulers with the
+        // producer and MMA warps, whose ~25 instructions per k-block then wait
+        // behind it: without the yields the MMA pace beside a running epilogue
+        // depends on how ptxas happens to pack this loop (550 to 985 cycles
+        // per k-block between two builds of the same source, r02n), with them
+        // it is ~515 (config 4 sustained 18.66 -> 17.93 ms).  NANOSLEEP 0 is
+        // the one instruction that deschedules a warp on request.
+        if constexpr (kF32EpiYield > 0) {
+            if ((k + 1) % kF32EpiYield == 0) asm volatile("nanosleep.u32 0;" ::: "memory");
+        }
     }
     store16<DIAG>(v, i, j0, p, out, ld, row_ok, vec_ok);
 }

@@ -33,10 +33,25 @@ def timed(fn, reps=3):
     return sorted(t)[len(t) // 2]
 
 
-res = {k: [] for k in orders}
-for r in range(int(os.environ.get("ROUNDS", "4"))):
+import time
+
+
+def sustained(fn, seconds=2.0):
+    fn(); torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); fn(); b.record(); b.synchronize()
+    reps = max(3, int(seconds * 1e3 / a.elapsed_time(b)))
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record(); b.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+# sustained (2 s back to back per order, alternating): on a power-capped GPU
+# only long windows compare to ~0.1%
+for r in range(int(os.environ.get("ROUNDS", "2"))):
     for k, t in orders.items():
-        res[k].append(timed(lambda: eng.compute(prep, None, dt, tiles=t, out=out, tile_major=True)))
-for k, v in res.items():
-    v = sorted(v)
-    print(f"config {cfg} {k}: fused median {v[len(v) // 2]:.3f} ms, min {v[0]:.3f} ({len(orders[k])} tiles)", flush=True)
+        ms = sustained(lambda: eng.compute(prep, None, dt, tiles=t, out=out, tile_major=True))
+        print(f"config {cfg} {k}: sustained {ms:.3f} ms/launch", flush=True)
+        time.sleep(2.0)
