@@ -500,12 +500,15 @@ def run_gpu(args):
         "kernel_ms": kern_ms,
         "kernel_share_of_step": kern_ms / step_ms,
     }
-    # the same fraction at the SM clock the timed region actually ran at: the
-    # peak is MACs/clk/SM x SMs x clock, and a power-capped step (sw_power_cap)
-    # runs below the clock the MMA-only probe holds
-    if clocks and clocks.get("sm_mhz") and peak_burst.get("sm_mhz"):
-        roofline["sm_mhz_timed_region"] = clocks["sm_mhz"]
-        roofline["frac_at_timed_clock"] = roofline["frac"] * peak_burst["sm_mhz"] / clocks["sm_mhz"]
+    # The same fraction at the SM clock the kernel is actually given: the peak
+    # is MACs/clk/SM x SMs x clock, and a power-capped run (sw_power_cap) sits
+    # below the clock the MMA-only probe holds.  Taken over the 2 s sustained
+    # section (NVML's clock lags: over the 20-step timed region it still shows
+    # the clock from before the load), whole steps, not the kernel alone.
+    if sustained and sustained.get("clocks") and sustained["clocks"].get("sm_mhz") and peak_burst.get("sm_mhz"):
+        f = 2.0 * W / (sustained["ms_per_step"] * 1e-3) / 1e12 / peak
+        sustained["frac_of_peak"] = f
+        sustained["frac_at_sustained_clock"] = f * peak_burst["sm_mhz"] / sustained["clocks"]["sm_mhz"]
 
     e2e = None
     if not args.no_e2e:
