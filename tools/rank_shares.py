@@ -15,6 +15,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="3,4")
 ap.add_argument("--worlds", default="2,4,8")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--sustained", type=float, default=0.0,
+                help="seconds: instead of timing ranks alone (cold, best of reps), run all ranks' steps of a world "
+                     "back to back for this long (same power state as the 1-rank run) and report "
+                     "T(1) / sum_r T_r: what the sharding itself costs (partial unpacks, round quantization)")
 a = ap.parse_args()
 eng = MIEngine.get(0)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=eng.device)
@@ -49,6 +53,30 @@ for cfg in [int(x) for x in a.configs.split(",")]:
         prep = eng.prepare(w, n, m, rank, world)
         eng.compute(prep, None, dt, tiles=tl, out=bufs[key], tile_major=True)
 
+    if a.sustained > 0:
+        def sus(fn):
+            fn(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); fn(); e1.record(); e1.synchronize()
+            reps = max(2, int(a.sustained * 1e3 / e0.elapsed_time(e1)))
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record(); e1.synchronize()
+            return e0.elapsed_time(e1) / reps
+
+        t1 = sus(lambda: step(0, 1))
+        print(json.dumps({"cfg": cfg, "world": 1, "sustained_ms": round(t1, 3)}), flush=True)
+        for world in [int(x) for x in a.worlds.split(",")]:
+            tw = sus(lambda: [step(r, world) for r in range(world)])
+            print(json.dumps({"cfg": cfg, "world": world, "sum_over_ranks_ms": round(tw, 3),
+                              "mean_rank_ms": round(tw / world, 3),
+                              "sharding_efficiency": round(t1 / tw, 3)}), flush=True)
+        t1b = sus(lambda: step(0, 1))
+        print(json.dumps({"cfg": cfg, "world": 1, "sustained_ms_again": round(t1b, 3)}), flush=True)
+        del bufs, w
+        torch.cuda.empty_cache()
+        continue
     t1 = timed(lambda: step(0, 1))
     print(json.dumps({"cfg": cfg, "world": 1, "ms": round(t1, 3)}), flush=True)
     for world in [int(x) for x in a.worlds.split(",")]:
