@@ -512,7 +512,11 @@ def run_gpu(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W, stages, buf)
+        try:
+            e2e = run_e2e(args, eng, words_dev, rank, world, n, m, cfg, out_dtype, W, stages, buf)
+        except Exception as exc:  # a failing end-to-end leg must not sink the device-resident line
+            e2e = {"value": None, "unit": UNIT, "error": f"{type(exc).__name__}: {exc}"}
+            print(f"[bench] rank {rank}: e2e leg failed: {exc}", file=sys.stderr, flush=True)
 
     tall = None
     if rank == 0 and world == 1 and not args.no_tall_narrow:
