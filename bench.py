@@ -267,12 +267,27 @@ def cpu_sample_text(n: int, m: int, ms: int, threads: int, extra: str = "") -> s
             f"(oracle/mi_oracle.c), OpenMP {threads} threads, host {O.cpu_model()}")
 
 
+def cpu_threads() -> int:
+    """Host threads of the CPU legs: every core this process may run on
+    (MI_BENCH_CPU_THREADS overrides).  Set explicitly: torchrun exports
+    OMP_NUM_THREADS=1 to its workers, which would turn the reference arm of an
+    N > 1 run into a single-thread baseline."""
+    env = os.environ.get("MI_BENCH_CPU_THREADS")
+    if env:
+        return max(1, int(env))
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):
+        return max(1, os.cpu_count() or 1)
+
+
 def cpu_baseline_leg(cfg: int, runs: int = 3) -> dict:
     """The oracle on the host cores, timed on the fixed sample (~10 s)."""
     from oracle import oracle as O
 
     words, n, m, ms = cpu_sample_words(cfg)
-    threads = O.c_num_threads()
+    threads = cpu_threads()
+    O.c_lib().oracle_set_threads(threads)
     O.c_mi_all_pairs(words, n)  # warm (threads, pages)
     times = []
     for _ in range(runs):
@@ -293,7 +308,8 @@ def run_reference(args):
     from oracle import oracle as O
 
     words, n, m, ms = cpu_sample_words(args.config)
-    threads = O.c_num_threads()
+    threads = cpu_threads()
+    O.c_lib().oracle_set_threads(threads)
     for _ in range(args.warmup):
         O.c_mi_all_pairs(words, n)
     times = []
